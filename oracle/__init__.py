@@ -39,7 +39,7 @@ def build(force: bool = False) -> str:
     """Compile oracle.c with gcc (plain -O2, IEEE semantics, no fast-math)."""
     src = os.path.join(_HERE, "oracle.c")
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
-        cmd = f"gcc -O2 -fPIC -shared -o {_LIB_PATH} {src} -lm -lpthread"
+        cmd = f"gcc -O2 -ffp-contract=off -fPIC -shared -o {_LIB_PATH} {src} -lm -lpthread"
         rc = os.system(cmd)
         if rc != 0:
             raise RuntimeError(f"oracle build failed: {cmd}")

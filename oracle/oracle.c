@@ -285,7 +285,7 @@ double oracle_loglik_rec(int D, int64_t n, const float* t, const int32_t* mark, 
  *   it = 0
  *   while it < max_iters:
  *     evaluate (lnL, grad) at p
- *     if non-finite: if no previous point or halvings == max_halvings -> DIVERGED (p <- previous
+ *     if non-finite: status |= NONFINITE; if no previous point or halvings == max_halvings -> DIVERGED (p <- previous
  *                    point if any), stop;  else p <- previous point, lr_w /= 2, halvings++,
  *                    it++, continue
  *     if tol_rel > 0 and it has a previous lnL: stall = (|lnL - prev| <= tol_rel*max(|prev|,1)) ? stall+1 : 0
@@ -337,9 +337,10 @@ int oracle_fit(int D, int64_t n, const float* t, const int32_t* mark, double T,
     while (it < cfg->max_iters) {
         double lnl = ll(D, n, t, mark, T, p, p + D, p + D + DD, g, g + D, g + D + DD, NULL);
         if (!isfinite(lnl) || !all_finite(g, P)) {
+            status |= OR_NONFINITE;
             if (!have_prev || halv >= cfg->max_halvings) {
                 if (have_prev) memcpy(p, prev, P * sizeof(double));
-                status |= OR_DIVERGED | OR_NONFINITE;
+                status |= OR_DIVERGED;
                 break;
             }
             memcpy(p, prev, P * sizeof(double));

@@ -1,0 +1,278 @@
+// abi.cu — the extern "C" boundary of libmdhp.so (include/mdhp.h): argument checks,
+// stream-ordered workspaces, error plumbing and the end-to-end host entry point.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include "common.cuh"
+
+namespace mdhp {
+
+
+int pack_launch(const mdhp_pack_desc* d, const double* t, const int32_t* mark,
+                const int64_t* win_off, const double* T, void* packed, int32_t* win_status,
+                cudaStream_t st);
+int loglik_launch(const Packed& P, const float* th, const float* al, const float* be, double* lnl,
+                  float* gt, float* ga, float* gb, const int32_t* status, cudaStream_t st);
+int fit_launch(const Packed& P, const FitCfgDev& cfg, float* th, float* al, float* be, float* opt,
+               double* lnl, int32_t* iters, int32_t* status, float* trace, int* counter,
+               cudaStream_t st);
+
+static thread_local char g_err[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launch(int k) { g_launches.fetch_add((uint64_t)k, std::memory_order_relaxed); }
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static int check_desc(const mdhp_pack_desc* d) {
+  if (!d) {
+    set_error("desc is NULL");
+    return MDHP_EINVAL;
+  }
+  if (d->D < 1 || d->D > 32) {
+    set_error("D=%d outside 1..32", d->D);
+    return MDHP_EDIM;
+  }
+  if (d->n_windows < 0 || d->n_events < 0) {
+    set_error("negative sizes (W=%lld, E=%lld)", (long long)d->n_windows, (long long)d->n_events);
+    return MDHP_EDIM;
+  }
+  if (d->time_mode < MDHP_TIME_RAW || d->time_mode > MDHP_TIME_EQ6) {
+    set_error("bad time_mode %d", d->time_mode);
+    return MDHP_EINVAL;
+  }
+  if (d->time_mode == MDHP_TIME_EQ6 && !(d->eq6_hi > d->eq6_lo)) {
+    set_error("EQ6 needs eq6_hi > eq6_lo (S:128)");
+    return MDHP_EINVAL;
+  }
+  return MDHP_OK;
+}
+
+static int check_cuda(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return MDHP_ECUDA;
+  }
+  return MDHP_OK;
+}
+
+static int check_cfg(const mdhp_fit_config* c) {
+  if (!c) {
+    set_error("cfg is NULL");
+    return MDHP_EINVAL;
+  }
+  if (c->max_iters < 0 || !(c->lr > 0.0f) || (c->optimizer != MDHP_OPT_GD && c->optimizer != MDHP_OPT_ADAM) ||
+      !(c->min_param > 0.0f) || c->patience < 0 || c->max_halvings < 0 ||
+      (c->optimizer == MDHP_OPT_ADAM && !(c->adam_b1 >= 0.0f && c->adam_b1 < 1.0f &&
+                                          c->adam_b2 >= 0.0f && c->adam_b2 < 1.0f && c->adam_eps >= 0.0f))) {
+    set_error("invalid fit config");
+    return MDHP_EINVAL;
+  }
+  return MDHP_OK;
+}
+
+}  // namespace mdhp
+
+using namespace mdhp;
+
+extern "C" {
+
+int32_t mdhp_version(void) { return 1; }
+
+const char* mdhp_last_error(void) { return g_err; }
+
+uint64_t mdhp_launch_count(void) { return g_launches.load(); }
+
+size_t mdhp_packed_bytes(const mdhp_pack_desc* d) {
+  if (check_desc(d) != MDHP_OK) return 0;
+  return make_layout(d->D, d->n_windows, d->n_events).total;
+}
+
+int mdhp_packed_layout(const mdhp_pack_desc* d, size_t* o) {
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!o) {
+    set_error("offsets is NULL");
+    return MDHP_EINVAL;
+  }
+  const Layout L = make_layout(d->D, d->n_windows, d->n_events);
+  const size_t v[14] = {L.begin, L.n, L.T32, L.perm, L.t32, L.dtp, L.mark, L.cnt, L.umax, L.mom,
+                        L.sort_cnt, L.total, (size_t)L.Epad, (size_t)L.Dp};
+  for (int k = 0; k < 14; k++) o[k] = v[k];
+  return MDHP_OK;
+}
+
+int mdhp_pack_windows(const mdhp_pack_desc* d, const double* t, const int32_t* mark,
+                      const int64_t* win_off, const double* T, void* packed, size_t packed_bytes,
+                      int32_t* win_status, void* stream) {
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!packed || !win_off || !T || !win_status || (d->n_events > 0 && (!t || !mark))) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  const size_t need = make_layout(d->D, d->n_windows, d->n_events).total;
+  if (packed_bytes < need) {
+    set_error("packed buffer too small: %zu < %zu", packed_bytes, need);
+    return MDHP_ESIZE;
+  }
+  rc = pack_launch(d, t, mark, win_off, T, packed, win_status, (cudaStream_t)stream);
+  if (rc) return rc;
+  return check_cuda("mdhp_pack_windows");
+}
+
+int mdhp_loglik_grad(const mdhp_pack_desc* d, const void* packed, const float* theta,
+                     const float* alpha, const float* beta, double* loglik, float* g_theta,
+                     float* g_alpha, float* g_beta, const int32_t* win_status, void* stream) {
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!packed || !theta || !alpha || !beta || !loglik || !win_status) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  const bool any = g_theta || g_alpha || g_beta, all = g_theta && g_alpha && g_beta;
+  if (any && !all) {
+    set_error("g_theta, g_alpha, g_beta must be all NULL or all non-NULL");
+    return MDHP_EINVAL;
+  }
+  const Layout L = make_layout(d->D, d->n_windows, d->n_events);
+  const Packed P = view(L, packed);
+  rc = loglik_launch(P, theta, alpha, beta, loglik, g_theta, g_alpha, g_beta, win_status,
+                     (cudaStream_t)stream);
+  if (rc) return rc;
+  return check_cuda("mdhp_loglik_grad");
+}
+
+int mdhp_fit(const mdhp_pack_desc* d, const void* packed, const mdhp_fit_config* cfg, float* theta,
+             float* alpha, float* beta, float* opt_state, double* loglik, int32_t* iters,
+             int32_t* win_status, float* lnl_trace, void* stream) {
+  int rc = check_desc(d);
+  if (rc) return rc;
+  rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (!packed || !theta || !alpha || !beta || !loglik || !iters || !win_status) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const Layout L = make_layout(d->D, d->n_windows, d->n_events);
+  const Packed P = view(L, packed);
+  const int64_t W = d->n_windows;
+  if (W == 0) return MDHP_OK;
+  const size_t PP = (size_t)d->D + 2 * (size_t)d->D * d->D;
+  // workspace: work counter (+ zero-initialised Adam moments when the caller passes none)
+  const bool own_opt = opt_state == nullptr && cfg->optimizer == MDHP_OPT_ADAM;
+  size_t ws_bytes = 256 + (own_opt ? sizeof(float) * 2 * PP * (size_t)W : 0);
+  void* ws = nullptr;
+  if (cudaMallocAsync(&ws, ws_bytes, st) != cudaSuccess) {
+    set_error("cudaMallocAsync(%zu) failed", ws_bytes);
+    return MDHP_ECUDA;
+  }
+  if (cudaMemsetAsync(ws, 0, ws_bytes, st) != cudaSuccess) {
+    cudaFreeAsync(ws, st);
+    set_error("cudaMemsetAsync failed");
+    return MDHP_ECUDA;
+  }
+  int* counter = static_cast<int*>(ws);
+  float* opt = own_opt ? reinterpret_cast<float*>(static_cast<char*>(ws) + 256) : opt_state;
+  FitCfgDev c;
+  c.max_iters = cfg->max_iters;
+  c.optimizer = cfg->optimizer;
+  c.loss_mean = cfg->loss_mean;
+  c.patience = cfg->patience;
+  c.max_halvings = cfg->max_halvings;
+  c.lr = cfg->lr;
+  c.b1 = cfg->adam_b1;
+  c.b2 = cfg->adam_b2;
+  c.eps = cfg->adam_eps;
+  c.tol_rel = cfg->tol_rel;
+  c.min_param = cfg->min_param;
+  c.fit_mask = cfg->fit_mask;
+  rc = fit_launch(P, c, theta, alpha, beta, opt, loglik, iters, win_status, lnl_trace, counter, st);
+  cudaFreeAsync(ws, st);
+  if (rc) return rc;
+  return check_cuda("mdhp_fit");
+}
+
+int mdhp_fit_host(const mdhp_pack_desc* d, const double* t_h, const int32_t* mark_h,
+                  const int64_t* off_h, const double* T_h, const mdhp_fit_config* cfg,
+                  float* theta_h, float* alpha_h, float* beta_h, double* lnl_h, int32_t* iters_h,
+                  int32_t* status_h, void* stream) {
+  int rc = check_desc(d);
+  if (rc) return rc;
+  rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (!off_h || !T_h || !theta_h || !alpha_h || !beta_h || !lnl_h || !iters_h || !status_h ||
+      (d->n_events > 0 && (!t_h || !mark_h))) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t W = d->n_windows, E = d->n_events;
+  const int D = d->D;
+  const size_t pk = make_layout(D, W, E).total;
+  const size_t bt = sizeof(double) * E, bm = sizeof(int32_t) * E, bo = sizeof(int64_t) * (W + 1),
+               bT = sizeof(double) * W, bth = sizeof(float) * W * D,
+               ba = sizeof(float) * W * D * D, bl = sizeof(double) * W, bi = sizeof(int32_t) * W;
+  size_t off[12];
+  size_t tot = 0;
+  const size_t sizes[11] = {bt, bm, bo, bT, bth, ba, ba, bl, bi, bi, pk};
+  for (int k = 0; k < 11; k++) {
+    off[k] = tot;
+    tot += align256(sizes[k]);
+  }
+  char* buf = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&buf), tot, st) != cudaSuccess) {
+    set_error("cudaMallocAsync(%zu) failed", tot);
+    return MDHP_ECUDA;
+  }
+  double* t_d = reinterpret_cast<double*>(buf + off[0]);
+  int32_t* m_d = reinterpret_cast<int32_t*>(buf + off[1]);
+  int64_t* o_d = reinterpret_cast<int64_t*>(buf + off[2]);
+  double* T_d = reinterpret_cast<double*>(buf + off[3]);
+  float* th_d = reinterpret_cast<float*>(buf + off[4]);
+  float* al_d = reinterpret_cast<float*>(buf + off[5]);
+  float* be_d = reinterpret_cast<float*>(buf + off[6]);
+  double* l_d = reinterpret_cast<double*>(buf + off[7]);
+  int32_t* it_d = reinterpret_cast<int32_t*>(buf + off[8]);
+  int32_t* s_d = reinterpret_cast<int32_t*>(buf + off[9]);
+  void* pk_d = buf + off[10];
+  auto h2d = [&](void* dst, const void* src, size_t n) {
+    return n == 0 || cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st) == cudaSuccess;
+  };
+  auto d2h = [&](void* dst, const void* src, size_t n) {
+    return n == 0 || cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+  };
+  bool ok = h2d(t_d, t_h, bt) && h2d(m_d, mark_h, bm) && h2d(o_d, off_h, bo) && h2d(T_d, T_h, bT) &&
+            h2d(th_d, theta_h, bth) && h2d(al_d, alpha_h, ba) && h2d(be_d, beta_h, ba);
+  if (!ok) {
+    cudaFreeAsync(buf, st);
+    set_error("host->device copy failed");
+    return MDHP_ECUDA;
+  }
+  rc = mdhp_pack_windows(d, t_d, m_d, o_d, T_d, pk_d, pk, s_d, stream);
+  if (!rc) rc = mdhp_fit(d, pk_d, cfg, th_d, al_d, be_d, nullptr, l_d, it_d, s_d, nullptr, stream);
+  if (!rc) {
+    ok = d2h(theta_h, th_d, bth) && d2h(alpha_h, al_d, ba) && d2h(beta_h, be_d, ba) &&
+         d2h(lnl_h, l_d, bl) && d2h(iters_h, it_d, bi) && d2h(status_h, s_d, bi);
+    if (!ok) {
+      set_error("device->host copy failed");
+      rc = MDHP_ECUDA;
+    }
+  }
+  cudaFreeAsync(buf, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && !rc) {
+    set_error("stream sync failed: %s", cudaGetErrorString(cudaGetLastError()));
+    rc = MDHP_ECUDA;
+  }
+  return rc;
+}
+
+}  // extern "C"

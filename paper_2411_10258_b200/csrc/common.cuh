@@ -1,0 +1,140 @@
+// common.cuh — packed layout and device helpers shared by the libmdhp kernels (sm_100a).
+// Nothing here is shared with oracle/ (DESIGN.md "Independence").
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+#include "../../include/mdhp.h"
+
+namespace mdhp {
+
+constexpr int kAlignEv = 8;     // window event ranges start on 8-event boundaries
+constexpr int kMom = 17;        // power moments m_1..m_17 of u/u_max per (window, mark)
+constexpr int kSortBuckets = 65536;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr unsigned kFull = 0xffffffffu;
+
+inline int pad_dims(int D) {
+  int p = 1;
+  while (p < D) p <<= 1;
+  return p;
+}
+
+__host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Byte layout of the packed buffer; a pure function of (D, W, E) so that every call can
+// recompute it from the descriptor (no device->host read of a header is ever needed).
+struct Layout {
+  int D, Dp;
+  int64_t W, E, Epad;
+  size_t begin, n, T32, perm, t32, dtp, mark, cnt, umax, mom, sort_cnt, total;
+};
+
+__host__ __device__ inline Layout make_layout(int D, int64_t W, int64_t E) {
+  Layout L;
+  L.D = D;
+  int p = 1;
+  while (p < D) p <<= 1;
+  L.Dp = p;
+  L.W = W;
+  L.E = E;
+  L.Epad = ((E + kAlignEv - 1) / kAlignEv) * kAlignEv + (int64_t)kAlignEv * W + kAlignEv;
+  size_t o = 0;
+  L.begin = o;    o = align256(o + sizeof(int64_t) * W);
+  L.n = o;        o = align256(o + sizeof(int32_t) * W);
+  L.T32 = o;      o = align256(o + sizeof(float) * W);
+  L.perm = o;     o = align256(o + sizeof(int32_t) * W);
+  L.t32 = o;      o = align256(o + sizeof(float) * L.Epad);
+  L.dtp = o;      o = align256(o + sizeof(float) * L.Epad);
+  L.mark = o;     o = align256(o + sizeof(uint8_t) * L.Epad);
+  L.cnt = o;      o = align256(o + sizeof(int32_t) * W * L.Dp);
+  L.umax = o;     o = align256(o + sizeof(float) * W * L.Dp);
+  L.mom = o;      o = align256(o + sizeof(float) * W * L.Dp * kMom);
+  L.sort_cnt = o; o = align256(o + sizeof(int32_t) * (kSortBuckets + 1));
+  L.total = o;
+  return L;
+}
+
+// Device view of a packed buffer.
+struct Packed {
+  const int64_t* begin;   // [W] first padded event slot of window w
+  const int32_t* n;       // [W] events
+  const float* T32;       // [W] horizon in analysis units
+  const int32_t* perm;    // [W] windows, longest first
+  const float* t32;       // [Epad]
+  const float* dtp;       // [Epad] gap to the previous event of the same mark (t + 1 if none)
+  const uint8_t* mark;    // [Epad]
+  const int32_t* cnt;     // [W][Dp]
+  const float* umax;      // [W][Dp] T - first event time of the mark (0 if none)
+  const float* mom;       // [W][Dp][kMom]
+  int64_t W;
+  int D, Dp;
+};
+
+inline Packed view(const Layout& L, const void* base) {
+  const char* b = static_cast<const char*>(base);
+  Packed P;
+  P.begin = reinterpret_cast<const int64_t*>(b + L.begin);
+  P.n = reinterpret_cast<const int32_t*>(b + L.n);
+  P.T32 = reinterpret_cast<const float*>(b + L.T32);
+  P.perm = reinterpret_cast<const int32_t*>(b + L.perm);
+  P.t32 = reinterpret_cast<const float*>(b + L.t32);
+  P.dtp = reinterpret_cast<const float*>(b + L.dtp);
+  P.mark = reinterpret_cast<const uint8_t*>(b + L.mark);
+  P.cnt = reinterpret_cast<const int32_t*>(b + L.cnt);
+  P.umax = reinterpret_cast<const float*>(b + L.umax);
+  P.mom = reinterpret_cast<const float*>(b + L.mom);
+  P.W = L.W;
+  P.D = L.D;
+  P.Dp = L.Dp;
+  return P;
+}
+
+// ---------------------------------------------------------------- device math (MUFU)
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2f(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcpf(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int DP>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int o = DP / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+template <int DP>
+__device__ __forceinline__ double group_sum_d(double v) {
+#pragma unroll
+  for (int o = DP / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+template <int DP>
+__device__ __forceinline__ int group_max_i(int v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+struct FitCfgDev {
+  int max_iters, optimizer, loss_mean, patience, max_halvings;
+  float lr, b1, b2, eps, tol_rel, min_param;
+  unsigned fit_mask;
+};
+
+// launch counter (process-wide), incremented by every launch site
+void count_launch(int k = 1);
+void set_error(const char* fmt, ...);
+
+}  // namespace mdhp
