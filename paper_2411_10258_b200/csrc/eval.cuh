@@ -3,10 +3,12 @@
 //
 // Mapping: a window is owned by a GROUP of DP lanes (DP = D padded to a power of two), so a
 // warp holds G = 32/DP windows.  Lane j of a group owns source column j for the row read and
-// target row j for the column update.  The per-window state lives in shared memory:
-//   K[i][j] = {alpha_ij, beta_ij, S_ij, Q'_ij}  (row stride DP+1 float4: conflict-free rows
-//                                                and columns)
-//   G[i][j] = {gR_ij, gQ_ij}                    gradient accumulators
+// target row j for the column update.  The per-window state lives in shared memory as three
+// float2 arrays (64-bit accesses are served per half-warp, so with an odd row stride DP+1 both
+// row and column accesses of a group are bank-conflict free; measured in profiles/):
+//   A[i][j]  = {alpha_ij, beta_ij}      parameters (row stride DP+1)
+//   SQ[i][j] = {S_ij, Q'_ij}            recurrence state (row stride DP+1)
+//   G[i][j]  = {gR_ij, gQ_ij}           gradient accumulators (row stride DP; rows only)
 // where S_ij = sum_{k in j} e^{-beta_ij (last_j - t_k)} is anchored at last_j, the time of the
 // latest event of source j, and Q'_ij = sum_{k in j} (last_j - t_k) e^{-beta_ij (last_j - t_k)}.
 //
@@ -43,29 +45,191 @@ __constant__ float c_inv_fact[kMom + 1] = {
 template <int DP>
 struct Smem {
   static constexpr int G = 32 / DP;                 // windows (groups) per warp
-  static constexpr int KS = DP * (DP + 1);          // float4 per group in K
-  static constexpr int GS = DP * DP;                // float2 per group in G
-  static constexpr size_t per_warp = (size_t)G * (KS * sizeof(float4) + GS * sizeof(float2));
+  static constexpr int RS = DP + 1;                 // row stride of A and SQ (float2 units)
+  static constexpr int AS = (DP + 1) * RS;          // float2 per group in A (and in SQ): DP real
+                                                    // rows + the null row DP
+  static constexpr int GS = (DP + 1) * DP;          // float2 per group in G (+ null row)
+  static constexpr int per_group = 2 * AS + GS;     // float2
+  static constexpr size_t per_warp = (size_t)G * per_group * sizeof(float2);
 };
 
-// Zero the dynamic state (S, Q', gR, gQ) of this lane's column j.
+// The null dimension DP.  A padding slot or the tail of a shorter window in the warp is the
+// event (t = -2, gap 0, mark DP).  With row DP = {alpha, beta} = {1, 0} at column 0 and {0, 0}
+// elsewhere, S_DP,0 = 1 and column DP's beta = 0, such an event reads lambda = 1 exactly
+// (lg2 = 0), never ties (t < every last >= -1), only touches column DP (never read by a real
+// row) and accumulates its gradient terms into the never-read row DP of G.  So the event loop
+// needs no per-event predicate.
+constexpr float kNullT = -2.0f;
+constexpr unsigned kNullMarks = 0xffffffffu;
+
+// Zero the dynamic state (S, Q', gR, gQ) of this lane's column j and its row-j entry of the
+// null column; (re)set the null row.
 template <int DP>
-__device__ __forceinline__ void reset_state(float4* K, float2* Gs, int j) {
+__device__ __forceinline__ void reset_state(float2* SQ, float2* Gs, int j) {
 #pragma unroll
   for (int i = 0; i < DP; i++) {
-    float4* p = &K[i * (DP + 1) + j];
-    p->z = 0.0f;
-    p->w = 0.0f;
+    SQ[i * (DP + 1) + j] = make_float2(0.0f, 0.0f);
     Gs[i * DP + j] = make_float2(0.0f, 0.0f);
   }
+  SQ[DP * (DP + 1) + j] = make_float2(j == 0 ? 1.0f : 0.0f, 0.0f);
+  SQ[j * (DP + 1) + DP] = make_float2(0.0f, 0.0f);
 }
+
+// Reduce-scatter of 8 per-lane values v[0..7] over the DP lanes of a group (DP >= 8): on
+// return v[0] holds the group sum of value e = (j >> (log2 DP - 3)) & 7.  8 shuffles for 8 sums
+// (DP = 16) instead of 8 x log2(DP) for 8 butterflies.
+template <int DP>
+__device__ __forceinline__ float reduce_scatter8(float (&v)[8], int j) {
+  {
+    const bool hi = (j & (DP / 2)) != 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const float mine = hi ? v[4 + k] : v[k];
+      const float oth = hi ? v[k] : v[4 + k];
+      v[k] = mine + __shfl_xor_sync(kFull, oth, DP / 2);
+    }
+  }
+  {
+    const bool hi = (j & (DP / 4)) != 0;
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const float mine = hi ? v[2 + k] : v[k];
+      const float oth = hi ? v[k] : v[2 + k];
+      v[k] = mine + __shfl_xor_sync(kFull, oth, DP / 4);
+    }
+  }
+  {
+    const bool hi = (j & (DP / 8)) != 0;
+    const float mine = hi ? v[1] : v[0];
+    const float oth = hi ? v[0] : v[1];
+    v[0] = mine + __shfl_xor_sync(kFull, oth, DP / 8);
+  }
+#pragma unroll
+  for (int o = DP / 16; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(kFull, v[0], o);
+  return v[0];
+}
+
+template <int DP>
+struct Log2 {
+  static constexpr int v = DP <= 1 ? 0 : 1 + Log2<DP / 2>::v;
+};
+template <>
+struct Log2<1> {
+  static constexpr int v = 0;
+};
 
 // The event loop of one window-evaluation.  All 32 lanes must call it (shuffles); groups whose
 // window has fewer events than `nmax` (the max over the warp) idle through the tail.
 // Returns via references: last (time of the latest event of source j), gth (sum 1/lambda over
-// events of mark j) and lsum (sum over events of lg2 lambda; identical in all lanes of a group).
+// events of mark j) and lsum (this lane's share of sum_n lg2 lambda_n; the group sum is the
+// total).
+//
+// DP >= 8 processes events in chunks of 8: pass 1 does the row reads and column updates of the
+// 8 events in order and keeps each event's partial sum alpha_ij R_ij (+ theta_i on lane i),
+// R_ij and Q_ij in registers; one reduce-scatter gives every lane the intensity of one event
+// (one rcp and one lg2 per lane per chunk instead of per event); pass 2 broadcasts w = 1/lambda
+// per event (1 shuffle) and accumulates the gradients.  DP <= 4 reduces each event directly.
+// 8 null events (t = kNullT, gap 0, mark 0xFF): chunks past a group's last event are read
+// from here, so every chunk load is unconditional (no predicated loads / default registers).
+__device__ __align__(32) float g_null_t[8] = {kNullT, kNullT, kNullT, kNullT,
+                                              kNullT, kNullT, kNullT, kNullT};
+__device__ __align__(32) float g_null_d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+__device__ __align__(8) uint8_t g_null_m[8] = {0xff, 0xff, 0xff, 0xff, 0xff, 0xff, 0xff, 0xff};
+
+struct Chunk {
+  float4 ta, tb, da, db;
+  uint2 mm;
+};
+
+__device__ __forceinline__ void load_chunk(Chunk& c, const float* t32, const float* dtp,
+                                           const uint8_t* mk, int64_t off, bool real) {
+  const float4* tp = reinterpret_cast<const float4*>(real ? t32 + off : g_null_t);
+  const float4* dp = reinterpret_cast<const float4*>(real ? dtp + off : g_null_d);
+  const uint2* mp = reinterpret_cast<const uint2*>(real ? mk + off : g_null_m);
+  c.ta = __ldg(tp);
+  c.tb = __ldg(tp + 1);
+  c.da = __ldg(dp);
+  c.db = __ldg(dp + 1);
+  c.mm = __ldg(mp);
+}
+
+// One chunk of 8 events (see event_loop).
 template <int DP, bool GRAD>
-__device__ __forceinline__ void event_loop(float4* __restrict__ K, float2* __restrict__ Gs,
+__device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __restrict__ A,
+                                              float2* __restrict__ SQ, float2* __restrict__ Gs,
+                                              const int j, const int gbase, const float th,
+                                              float& last, float& gth, double& lsum) {
+  constexpr int RS = DP + 1;
+  constexpr int LG = Log2<DP>::v;
+  const int colb = j * RS;
+  float pv[8], Rv[8], Qv[8];
+  float lacc = 0.0f;
+#pragma unroll
+  for (int s = 0; s < 8; s++) {
+    const float t = s == 0 ? ck.ta.x : s == 1 ? ck.ta.y : s == 2 ? ck.ta.z : s == 3 ? ck.ta.w
+                  : s == 4 ? ck.tb.x : s == 5 ? ck.tb.y : s == 6 ? ck.tb.z : ck.tb.w;
+    const float dc = s == 0 ? ck.da.x : s == 1 ? ck.da.y : s == 2 ? ck.da.z : s == 3 ? ck.da.w
+                   : s == 4 ? ck.db.x : s == 5 ? ck.db.y : s == 6 ? ck.db.z : ck.db.w;
+    const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
+    const int i = min((int)((word >> (8 * (s & 3))) & 0xffu), DP);
+    const float2 ar = A[i * RS + j];
+    const float2 sr = SQ[i * RS + j];
+    const float bc = A[colb + i].y;
+    const float2 sc = SQ[colb + i];
+    const float dr = t - last;
+    const float er = ex2f(ar.y * (dr * -kLog2e));
+    const float ec = ex2f(bc * (dc * -kLog2e));
+    const float R = fmaf(er, sr.x, (dr == 0.0f) ? -1.0f : 0.0f);  // strict T_j^k < t
+    const bool own = i == j;
+    const float p = fmaf(ar.x, R, own ? th : 0.0f);     // theta_i enters through lane i
+    SQ[colb + i] = make_float2(fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
+    last = own ? t : last;
+    if constexpr (DP >= 8) {
+      pv[s] = p;
+      if (GRAD) {
+        Rv[s] = R;
+        Qv[s] = er * fmaf(dr, sr.x, sr.y);
+      }
+    } else {
+      const float lam = group_sum<DP>(p);
+      if (GRAD) {
+        const float w = rcpf(lam);
+        float2 gg = Gs[i * DP + j];
+        gg.x = fmaf(R, w, gg.x);
+        gg.y = fmaf(er * fmaf(dr, sr.x, sr.y), w, gg.y);
+        Gs[i * DP + j] = gg;
+        gth += own ? w : 0.0f;
+      }
+      lacc += (j == 0) ? lg2f(lam) : 0.0f;
+    }
+    __syncwarp();
+  }
+  if constexpr (DP >= 8) {
+    const float lam = reduce_scatter8<DP>(pv, j);
+    if ((j & ((DP >> 3) - 1)) == 0) lacc += lg2f(lam);
+    if (GRAD) {
+      const float w = rcpf(lam);
+#pragma unroll
+      for (int s = 0; s < 8; s++) {
+        const float ws = __shfl_sync(kFull, w, gbase + (s << (LG - 3)));
+        const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
+        const int i = min((int)((word >> (8 * (s & 3))) & 0xffu), DP);
+        float2 gg = Gs[i * DP + j];
+        gg.x = fmaf(Rv[s], ws, gg.x);
+        gg.y = fmaf(Qv[s], ws, gg.y);
+        Gs[i * DP + j] = gg;
+        gth += (i == j) ? ws : 0.0f;
+      }
+    }
+  }
+  lsum += (double)lacc;
+}
+
+// The event loop of one window-evaluation, two chunks per iteration with explicit buffers so
+// the prefetch of chunk c+1 overlaps chunk c without register rotation.
+template <int DP, bool GRAD>
+__device__ __forceinline__ void event_loop(const float2* __restrict__ A, float2* __restrict__ SQ,
+                                           float2* __restrict__ Gs,
                                            const int j, const int gbase,
                                            const float* __restrict__ t32,
                                            const float* __restrict__ dtp,
@@ -75,73 +239,14 @@ __device__ __forceinline__ void event_loop(float4* __restrict__ K, float2* __res
   last = -1.0f;
   gth = 0.0f;
   lsum = 0.0;
-  float4 ta = make_float4(0, 0, 0, 0), tb = ta, da = ta, db = ta;
-  uint2 mm = make_uint2(0, 0);
-  if (n > 0) {
-    const float4* tp = reinterpret_cast<const float4*>(t32 + beg);
-    const float4* dp = reinterpret_cast<const float4*>(dtp + beg);
-    ta = __ldg(tp);
-    tb = __ldg(tp + 1);
-    da = __ldg(dp);
-    db = __ldg(dp + 1);
-    mm = __ldg(reinterpret_cast<const uint2*>(mk + beg));
-  }
-  for (int base = 0; base < nmax; base += 8) {
-    // prefetch the next chunk of 8 events (broadcast loads: every lane of the group reads
-    // the same 16-byte words; L1/L2 resident across fit iterations)
-    float4 nta = ta, ntb = tb, nda = da, ndb = db;
-    uint2 nmm = mm;
-    if (base + 8 < n) {
-      const float4* tp = reinterpret_cast<const float4*>(t32 + beg + base + 8);
-      const float4* dp = reinterpret_cast<const float4*>(dtp + beg + base + 8);
-      nta = __ldg(tp);
-      ntb = __ldg(tp + 1);
-      nda = __ldg(dp);
-      ndb = __ldg(dp + 1);
-      nmm = __ldg(reinterpret_cast<const uint2*>(mk + beg + base + 8));
-    }
-    float lacc = 0.0f;
-#pragma unroll
-    for (int s = 0; s < 8; s++) {
-      const bool act = base + s < n;
-      const float t = s == 0 ? ta.x : s == 1 ? ta.y : s == 2 ? ta.z : s == 3 ? ta.w
-                    : s == 4 ? tb.x : s == 5 ? tb.y : s == 6 ? tb.z : tb.w;
-      const float dc = s == 0 ? da.x : s == 1 ? da.y : s == 2 ? da.z : s == 3 ? da.w
-                     : s == 4 ? db.x : s == 5 ? db.y : s == 6 ? db.z : db.w;
-      const unsigned word = s < 4 ? mm.x : mm.y;
-      int i = (int)((word >> (8 * (s & 3))) & 0xffu);
-      i = act ? i : 0;
-      const float4 kr = K[i * (DP + 1) + j];
-      const float4 kc = K[j * (DP + 1) + i];
-      const float dr = t - last;
-      const float er = ex2f(kr.y * (dr * -kLog2e));
-      const float ec = ex2f(kc.y * (dc * -kLog2e));
-      const float tie = (dr == 0.0f) ? 1.0f : 0.0f;
-      const float R = fmaf(er, kr.z, -tie);
-      float p = kr.x * R;
-      p = group_sum<DP>(p);
-      const float lam = p + __shfl_sync(kFull, th, gbase + i);
-      if (GRAD) {
-        const float Q = er * fmaf(dr, kr.z, kr.w);
-        const float w = rcpf(lam);
-        float2 gg = Gs[i * DP + j];
-        gg.x = fmaf(R, w, gg.x);
-        gg.y = fmaf(Q, w, gg.y);
-        if (act) Gs[i * DP + j] = gg;
-        gth += (act && i == j) ? w : 0.0f;
-      }
-      lacc += act ? lg2f(lam) : 0.0f;
-      const float Sn = fmaf(ec, kc.z, 1.0f);
-      const float Qn = ec * fmaf(dc, kc.z, kc.w);
-      if (act) {
-        float2* pc = reinterpret_cast<float2*>(&K[j * (DP + 1) + i]) + 1;
-        *pc = make_float2(Sn, Qn);
-        if (i == j) last = t;
-      }
-      __syncwarp();
-    }
-    lsum += (double)lacc;
-    ta = nta; tb = ntb; da = nda; db = ndb; mm = nmm;
+  Chunk c0, c1;
+  load_chunk(c0, t32, dtp, mk, beg, n > 0);
+  for (int base = 0; base < nmax; base += 16) {
+    load_chunk(c1, t32, dtp, mk, beg + base + 8, base + 8 < n);
+    process_chunk<DP, GRAD>(c0, A, SQ, Gs, j, gbase, th, last, gth, lsum);
+    if (base + 8 >= nmax) break;
+    load_chunk(c0, t32, dtp, mk, beg + base + 16, base + 16 < n);
+    process_chunk<DP, GRAD>(c1, A, SQ, Gs, j, gbase, th, last, gth, lsum);
   }
 }
 

@@ -22,17 +22,17 @@ struct WarpCtx {
 // Writes gradients (d alpha, d beta) over the accumulators in Gs when GRAD; returns lnL
 // (identical in every lane of the group) and this lane's d theta_j.
 template <int DP, bool GRAD>
-__device__ __forceinline__ double eval_window(const Packed& P, float4* K, float2* Gs,
+__device__ __forceinline__ double eval_window(const Packed& P, float2* A, float2* SQ, float2* Gs,
                                               const WarpCtx<DP>& c, int64_t w, bool live,
                                               int nmax, float th, const ColInfo& ci,
                                               float& dth, bool& finite) {
-  reset_state<DP>(K, Gs, c.j);
+  reset_state<DP>(SQ, Gs, c.j);
   __syncwarp();
   const int n = live ? P.n[w] : 0;
   const int64_t beg = live ? P.begin[w] : 0;
   float last, gth;
   double lsum;
-  event_loop<DP, GRAD>(K, Gs, c.j, c.gbase, P.t32, P.dtp, P.mark, beg, n, nmax, th, last, gth,
+  event_loop<DP, GRAD>(A, SQ, Gs, c.j, c.gbase, P.t32, P.dtp, P.mark, beg, n, nmax, th, last, gth,
                        lsum);
   ColInfo cc = ci;
   cc.last = last;
@@ -42,9 +42,10 @@ __device__ __forceinline__ double eval_window(const Packed& P, float4* K, float2
   bool ok = true;
 #pragma unroll 4
   for (int i = 0; i < DP; i++) {
-    float4 k = K[i * (DP + 1) + c.j];
+    const float2 k = A[i * (DP + 1) + c.j];
+    const float2 sq = SQ[i * (DP + 1) + c.j];
     float Eb, Hb2;
-    compensator(cc, S, k.y, k.z, k.w, Eb, Hb2);
+    compensator(cc, S, k.y, sq.x, sq.y, Eb, Hb2);
     if (cc.real && i < P.D) {
       part3 += (double)(k.x * Eb);
       if (GRAD) {
@@ -59,6 +60,7 @@ __device__ __forceinline__ double eval_window(const Packed& P, float4* K, float2
   dth = gth - ci.T;
   if (GRAD && cc.real) ok = ok && isfinite(dth);
   part3 = group_sum_d<DP>(part3);
+  lsum = group_sum_d<DP>(lsum);
   const double sth = group_sum_d<DP>(cc.real ? (double)th : 0.0);
   const double lnl = (double)kLn2 * lsum + part3 - (double)ci.T * sth;
   const unsigned bal = __ballot_sync(kFull, ok) & c.gmask;
@@ -79,7 +81,7 @@ __device__ __forceinline__ ColInfo col_info(const Packed& P, int64_t w, bool liv
 
 // Load window parameters into K (alpha, beta) and return theta_j (0 for padded lanes).
 template <int DP>
-__device__ __forceinline__ float load_params(float4* K, const WarpCtx<DP>& c, int D, int64_t w,
+__device__ __forceinline__ float load_params(float2* A, const WarpCtx<DP>& c, int D, int64_t w,
                                              bool live, const float* __restrict__ theta,
                                              const float* __restrict__ alpha,
                                              const float* __restrict__ beta) {
@@ -91,15 +93,16 @@ __device__ __forceinline__ float load_params(float4* K, const WarpCtx<DP>& c, in
       a = alpha[(size_t)w * D * D + (size_t)i * D + c.j];
       b = beta[(size_t)w * D * D + (size_t)i * D + c.j];
     }
-    float4* p = &K[i * (DP + 1) + c.j];
-    p->x = a;
-    p->y = b;
+    A[i * (DP + 1) + c.j] = make_float2(a, b);
   }
+  // null dimension (see eval.cuh): row DP = {1,0} at column 0, column DP has beta = 0
+  A[DP * (DP + 1) + c.j] = make_float2(c.j == 0 ? 1.0f : 0.0f, 0.0f);
+  A[c.j * (DP + 1) + DP] = make_float2(0.0f, 0.0f);
   return real ? theta[(size_t)w * D + c.j] : 0.0f;
 }
 
 template <int DP>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, DP >= 32 ? 2 : 4)
 k_loglik(Packed P, const float* __restrict__ theta, const float* __restrict__ alpha,
          const float* __restrict__ beta, double* __restrict__ lnl_out,
          float* __restrict__ g_theta, float* __restrict__ g_alpha, float* __restrict__ g_beta,
@@ -108,23 +111,24 @@ k_loglik(Packed P, const float* __restrict__ theta, const float* __restrict__ al
   using SM = Smem<DP>;
   WarpCtx<DP> c;
   const int wid = threadIdx.x >> 5;
-  unsigned char* wbase = smem + wid * SM::per_warp;
-  float4* K = reinterpret_cast<float4*>(wbase) + c.g * SM::KS;
-  float2* Gs = reinterpret_cast<float2*>(wbase + SM::G * SM::KS * sizeof(float4)) + c.g * SM::GS;
+  float2* gbase_s = reinterpret_cast<float2*>(smem + wid * SM::per_warp) + c.g * SM::per_group;
+  float2* A = gbase_s;
+  float2* SQ = gbase_s + SM::AS;
+  float2* Gs = gbase_s + 2 * SM::AS;
   const int64_t unit = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
   const int64_t slot = unit * SM::G + c.g;
   const int64_t w = slot < P.W ? P.perm[slot] : 0;
   const bool live = slot < P.W && !(status[w] & MDHP_ST_INVALID);
   const int D = P.D;
-  const float th = load_params<DP>(K, c, D, w, live, theta, alpha, beta);
+  const float th = load_params<DP>(A, c, D, w, live, theta, alpha, beta);
   const ColInfo ci = col_info<DP>(P, w, live, c.j);
   const int nmax = group_max_i<DP>(live ? P.n[w] : 0);
   float dth;
   bool finite;
   const bool grad = g_theta != nullptr;
   double lnl;
-  if (grad) lnl = eval_window<DP, true>(P, K, Gs, c, w, live, nmax, th, ci, dth, finite);
-  else lnl = eval_window<DP, false>(P, K, Gs, c, w, live, nmax, th, ci, dth, finite);
+  if (grad) lnl = eval_window<DP, true>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite);
+  else lnl = eval_window<DP, false>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite);
   if (slot >= P.W) return;
   if (c.j == 0) lnl_out[w] = live ? lnl : (double)NAN;
   if (grad && c.j < D) {
@@ -141,7 +145,7 @@ k_loglik(Packed P, const float* __restrict__ theta, const float* __restrict__ al
 // semantics, then projection.  Gradients of lnL are in Gs (alpha, beta) and
 // dth; the loss gradient is -grad * scale.
 template <int DP>
-__device__ __forceinline__ void step_column(float4* K, const float2* Gs, const WarpCtx<DP>& c,
+__device__ __forceinline__ void step_column(float2* A, const float2* Gs, const WarpCtx<DP>& c,
                                             int D, int64_t w, const FitCfgDev& cfg, float lr_w,
                                             int s, float scale, float dth, float& th,
                                             float* __restrict__ opt) {
@@ -171,7 +175,7 @@ __device__ __forceinline__ void step_column(float4* K, const float2* Gs, const W
   };
   if (cfg.fit_mask & MDHP_FIT_THETA) th = upd(th, dth, (size_t)c.j, cfg.min_param);
   for (int i = 0; i < D; i++) {
-    float4* k = &K[i * (DP + 1) + c.j];
+    float2* k = &A[i * (DP + 1) + c.j];
     const float2 gg = Gs[i * DP + c.j];
     const size_t q = (size_t)D + (size_t)i * D + c.j;
     if (cfg.fit_mask & MDHP_FIT_ALPHA) k->x = upd(k->x, gg.x, q, 0.0f);
@@ -180,13 +184,13 @@ __device__ __forceinline__ void step_column(float4* K, const float2* Gs, const W
 }
 
 template <int DP>
-__device__ __forceinline__ void store_params(const float4* K, const WarpCtx<DP>& c, int D,
+__device__ __forceinline__ void store_params(const float2* A, const WarpCtx<DP>& c, int D,
                                              int64_t w, float th, float* __restrict__ theta,
                                              float* __restrict__ alpha, float* __restrict__ beta) {
   if (c.j >= D) return;
   theta[(size_t)w * D + c.j] = th;
   for (int i = 0; i < D; i++) {
-    const float4 k = K[i * (DP + 1) + c.j];
+    const float2 k = A[i * (DP + 1) + c.j];
     alpha[(size_t)w * D * D + (size_t)i * D + c.j] = k.x;
     beta[(size_t)w * D * D + (size_t)i * D + c.j] = k.y;
   }
@@ -196,7 +200,7 @@ __device__ __forceinline__ void store_params(const float4* K, const WarpCtx<DP>&
 // counter and runs their whole iteration loop on chip (a6), then evaluates lnL at the final
 // parameters and writes everything back.
 template <int DP>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, DP >= 32 ? 2 : 4)
 k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ alpha,
       float* __restrict__ beta, float* __restrict__ opt, double* __restrict__ lnl_out,
       int32_t* __restrict__ iters_out, int32_t* __restrict__ status,
@@ -205,9 +209,10 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
   using SM = Smem<DP>;
   WarpCtx<DP> c;
   const int wid = threadIdx.x >> 5;
-  unsigned char* wbase = smem + wid * SM::per_warp;
-  float4* K = reinterpret_cast<float4*>(wbase) + c.g * SM::KS;
-  float2* Gs = reinterpret_cast<float2*>(wbase + SM::G * SM::KS * sizeof(float4)) + c.g * SM::GS;
+  float2* gbase_s = reinterpret_cast<float2*>(smem + wid * SM::per_warp) + c.g * SM::per_group;
+  float2* A = gbase_s;
+  float2* SQ = gbase_s + SM::AS;
+  float2* Gs = gbase_s + 2 * SM::AS;
   const int D = P.D;
   const int64_t nunits = (P.W + SM::G - 1) / SM::G;
   for (;;) {
@@ -219,7 +224,7 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
     const int64_t w = slot < P.W ? P.perm[slot] : 0;
     const int st0 = slot < P.W ? status[w] : MDHP_ST_INVALID;
     const bool live = slot < P.W && !(st0 & MDHP_ST_INVALID);
-    float th = load_params<DP>(K, c, D, w, live, theta, alpha, beta);
+    float th = load_params<DP>(A, c, D, w, live, theta, alpha, beta);
     const ColInfo ci = col_info<DP>(P, w, live, c.j);
     const int n = live ? P.n[w] : 0;
     const float scale = (cfg.loss_mean && n > 0) ? 1.0f / (float)n : 1.0f;
@@ -233,16 +238,16 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
       const int nmax = group_max_i<DP>(done ? 0 : n);
       float dth;
       bool finite;
-      const double lnl = eval_window<DP, true>(P, K, Gs, c, w, !done, nmax, th, ci, dth, finite);
+      const double lnl = eval_window<DP, true>(P, A, SQ, Gs, c, w, !done, nmax, th, ci, dth, finite);
       if (!done) {
         if (!finite) {
           st |= MDHP_ST_NONFINITE;
           if (!have_prev || halv >= cfg.max_halvings) {
             st |= MDHP_ST_DIVERGED;
             done = true;
-            if (have_prev) th = load_params<DP>(K, c, D, w, true, theta, alpha, beta);
+            if (have_prev) th = load_params<DP>(A, c, D, w, true, theta, alpha, beta);
           } else {
-            th = load_params<DP>(K, c, D, w, true, theta, alpha, beta);
+            th = load_params<DP>(A, c, D, w, true, theta, alpha, beta);
             lr_w *= 0.5f;
             halv++;
             it++;
@@ -260,10 +265,10 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
           if (!done) {
             lnl_prev = lnl;
             have_lnl = true;
-            store_params<DP>(K, c, D, w, th, theta, alpha, beta);   // previous point
+            store_params<DP>(A, c, D, w, th, theta, alpha, beta);   // previous point
             have_prev = true;
             s++;
-            step_column<DP>(K, Gs, c, D, w, cfg, lr_w, s, scale, dth, th, opt);
+            step_column<DP>(A, Gs, c, D, w, cfg, lr_w, s, scale, dth, th, opt);
             it++;
           }
         }
@@ -275,9 +280,9 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
     const int nmax = group_max_i<DP>(n);
     float dth;
     bool finite;
-    const double lnl = eval_window<DP, false>(P, K, Gs, c, w, live, nmax, th, ci, dth, finite);
+    const double lnl = eval_window<DP, false>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite);
     if (slot < P.W) {
-      if (live) store_params<DP>(K, c, D, w, th, theta, alpha, beta);
+      if (live) store_params<DP>(A, c, D, w, th, theta, alpha, beta);
       if (c.j == 0) {
         lnl_out[w] = live ? lnl : (double)NAN;
         iters_out[w] = it;

@@ -106,8 +106,8 @@ k_pack_events(int D, int Dp, int mode, double lo, double hi, int64_t W,
   st = __reduce_or_sync(kFull, st);
   if (st & (MDHP_ST_UNSORTED | MDHP_ST_BAD_MARK)) st &= ~MDHP_ST_SAME_DIM_TIE;
   const int64_t npad = round8(n);
-  for (int64_t k = n + lane; k < npad; k += 32) {
-    o_t32[beg + k] = T32;
+  for (int64_t k = n + lane; k < npad; k += 32) {   // null events (eval.cuh: kNullT)
+    o_t32[beg + k] = -2.0f;
     o_dtp[beg + k] = 0.0f;
     o_mark[beg + k] = 0xFF;
   }
