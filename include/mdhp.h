@@ -188,6 +188,43 @@ int mdhp_fit_host(const mdhp_pack_desc* desc, const double* t_host, const int32_
                   float* beta_host, double* loglik_host, int32_t* iters_host,
                   int32_t* win_status_host, void* stream);
 
+/* ---------------------------------------------------------------- long single sequences (a7)
+ * One long marked sequence on [0, T] (e.g. BASELINE config 4: D = 16, 1e6 events over 1000 s),
+ * evaluated and fitted by a chunked parallel scan: the sequence is cut into chunks of about
+ * chunk_events events (never inside a group of equal times), each chunk's times are stored
+ * relative to its base (the previous chunk's last event; fp64 difference rounded to fp32, so
+ * resolution stays ~1e-7 s), chunk-local decayed states are combined by an exclusive scan of
+ * their affine maps (S <- e^{-beta L} S + S_loc, Q <- e^{-beta L}(Q + L S) + Q_loc), and every
+ * chunk then re-runs the event loop from its carried-in state.  Same Eq.(5) lnL and gradients
+ * as mdhp_loglik_grad (row a7).  Times are RAW (seconds).             */
+typedef struct {
+    int32_t D;             /* 1..32                                                         */
+    int32_t chunk_events;  /* >= 8; 256 is a good default                                   */
+    int64_t n_events;      /* N >= 0                                                         */
+    double  T;             /* horizon T_span > 0                                             */
+} mdhp_seq_desc;
+
+size_t mdhp_seq_packed_bytes(const mdhp_seq_desc* desc);
+
+/* t [N] fp64 non-decreasing in [0, T], mark [N] int32 in 0..D-1 (device).  status [1] int32
+ * (device) receives the MDHP_ST_* validation bits.  Asynchronous.                          */
+int mdhp_seq_pack(const mdhp_seq_desc* desc, const double* t, const int32_t* mark,
+                  void* packed, size_t packed_bytes, int32_t* status, void* stream);
+
+/* theta [D], alpha [D][D], beta [D][D] fp32; loglik [1] fp64; g_* as in mdhp_loglik_grad
+ * (all NULL -> lnL only).  NaN outputs for an invalid sequence.  Asynchronous.              */
+int mdhp_seq_loglik_grad(const mdhp_seq_desc* desc, const void* packed, const float* theta,
+                         const float* alpha, const float* beta, double* loglik, float* g_theta,
+                         float* g_alpha, float* g_beta, void* stream);
+
+/* The loop of mdhp_fit for one sequence: per iteration 3 scan phases + reduce + one fused
+ * epilogue/step kernel; the stop/rollback state lives on the device (no host sync).
+ * opt_state [2][D + 2 D^2] or NULL; loglik [1]; iters [1]; status [1] out; lnl_trace
+ * [max_iters] or NULL.  Asynchronous.                                                      */
+int mdhp_seq_fit(const mdhp_seq_desc* desc, const void* packed, const mdhp_fit_config* cfg,
+                 float* theta, float* alpha, float* beta, float* opt_state, double* loglik,
+                 int32_t* iters, int32_t* status, float* lnl_trace, void* stream);
+
 /* Byte offsets of the packed sections (introspection for tests/tools), in this order:
  * [0] begin i64[W]  [1] n i32[W]  [2] T32 f32[W]  [3] perm i32[W]  [4] t32 f32[Epad]
  * [5] dtp f32[Epad] [6] mark u8[Epad]  [7] cnt i32[W][Dp]  [8] umax f32[W][Dp]

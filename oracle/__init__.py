@@ -128,8 +128,13 @@ def convert_window(D, t, mark, T, time_mode=TIME_RAW, lo=0.0, hi=1.0):
     return out, float(T32[0]), int(st)
 
 
+def _times(t):
+    """Times as fp64: fp32 analysis times are promoted exactly; fp64 times pass through."""
+    return np.ascontiguousarray(np.asarray(t), dtype=np.float64)
+
+
 def _ll(fn, D, t32, mark, T, theta, alpha, beta, grads=True):
-    t32 = np.ascontiguousarray(t32, dtype=np.float32)
+    t32 = _times(t32)
     mark = np.ascontiguousarray(mark, dtype=np.int32)
     theta, alpha, beta = _f64(theta).ravel(), _f64(alpha).ravel(), _f64(beta).ravel()
     gt = np.zeros(D) if grads else None
@@ -155,7 +160,7 @@ def loglik_rec(D, t32, mark, T, theta, alpha, beta, grads=True):
 
 
 def fit(D, t32, mark, T, theta, alpha, beta, cfg: FitConfig, trace=False):
-    t32 = np.ascontiguousarray(t32, dtype=np.float32)
+    t32 = _times(t32)
     mark = np.ascontiguousarray(mark, dtype=np.int32)
     th, al, be = _f64(theta).ravel().copy(), _f64(alpha).ravel().copy(), _f64(beta).ravel().copy()
     lnl = np.zeros(1)
@@ -175,7 +180,7 @@ def loglik_batch(D, t32, mark, win_off, T, theta, alpha, beta, nthreads=None, us
                  grads=True):
     W = len(win_off) - 1
     nthreads = nthreads or os.cpu_count() or 1
-    t32 = np.ascontiguousarray(t32, dtype=np.float32)
+    t32 = _times(t32)
     mark = np.ascontiguousarray(mark, dtype=np.int32)
     off = np.ascontiguousarray(win_off, dtype=np.int64)
     T = _f64(T)
@@ -193,7 +198,7 @@ def loglik_batch(D, t32, mark, win_off, T, theta, alpha, beta, nthreads=None, us
 def fit_batch(D, t32, mark, win_off, T, theta, alpha, beta, cfg: FitConfig, nthreads=None):
     W = len(win_off) - 1
     nthreads = nthreads or os.cpu_count() or 1
-    t32 = np.ascontiguousarray(t32, dtype=np.float32)
+    t32 = _times(t32)
     mark = np.ascontiguousarray(mark, dtype=np.int32)
     off = np.ascontiguousarray(win_off, dtype=np.int64)
     T = _f64(T)

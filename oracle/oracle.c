@@ -24,8 +24,8 @@
  *   *_batch                the same over many windows, on a pthread pool.
  *
  * Conventions: alpha, beta are D*D row-major [i][j] = target i, source j (Eq.(2) P:107:
- * lambda^i sums over sources j).  theta is length D.  Times are the fp32 analysis times
- * produced by oracle_convert_window, promoted to double.
+ * lambda^i sums over sources j).  theta is length D.  Times are fp64: the fp32 analysis times
+ * produced by oracle_convert_window promoted exactly, or raw fp64 times (long sequences).
  */
 #include <math.h>
 #include <float.h>
@@ -127,7 +127,7 @@ int oracle_convert_window(int D, int time_mode, double lo, double hi, int64_t n,
  * gamma_out (optional) receives Gamma of App. B = T sum theta - Part3.
  * Any gradient pointer may be NULL.
  * ------------------------------------------------------------------------------------- */
-double oracle_loglik_def(int D, int64_t n, const float* t, const int32_t* mark, double T,
+double oracle_loglik_def(int D, int64_t n, const double* t, const int32_t* mark, double T,
                          const double* theta, const double* alpha, const double* beta,
                          double* g_theta, double* g_alpha, double* g_beta, double* gamma_out)
 {
@@ -200,7 +200,7 @@ double oracle_loglik_def(int D, int64_t n, const float* t, const int32_t* mark, 
  * event as in oracle_loglik_def (expm1), not as R(T) - N.
  * Same outputs as oracle_loglik_def.
  * ------------------------------------------------------------------------------------- */
-double oracle_loglik_rec(int D, int64_t n, const float* t, const int32_t* mark, double T,
+double oracle_loglik_rec(int D, int64_t n, const double* t, const int32_t* mark, double T,
                          const double* theta, const double* alpha, const double* beta,
                          double* g_theta, double* g_alpha, double* g_beta, double* gamma_out)
 {
@@ -311,7 +311,7 @@ static int all_finite(const double* x, size_t n) {
     return 1;
 }
 
-int oracle_fit(int D, int64_t n, const float* t, const int32_t* mark, double T,
+int oracle_fit(int D, int64_t n, const double* t, const int32_t* mark, double T,
                const oracle_fit_cfg* cfg, double* theta, double* alpha, double* beta,
                double* lnl_out, int32_t* iters_out, double* trace)
 {
@@ -325,7 +325,7 @@ int oracle_fit(int D, int64_t n, const float* t, const int32_t* mark, double T,
     memcpy(p, theta, D * sizeof(double));
     memcpy(p + D, alpha, DD * sizeof(double));
     memcpy(p + D + DD, beta, DD * sizeof(double));
-    double (*ll)(int, int64_t, const float*, const int32_t*, double, const double*, const double*,
+    double (*ll)(int, int64_t, const double*, const int32_t*, double, const double*, const double*,
                  const double*, double*, double*, double*, double*) =
         cfg->use_def ? oracle_loglik_def : oracle_loglik_rec;
 
@@ -392,7 +392,7 @@ int oracle_fit(int D, int64_t n, const float* t, const int32_t* mark, double T,
 typedef struct {
     int kind;            /* 0 = loglik (rec), 1 = loglik (def), 2 = fit */
     int D; int64_t W;
-    const float* t; const int32_t* mark; const int64_t* off; const double* T;
+    const double* t; const int32_t* mark; const int64_t* off; const double* T;
     double *theta, *alpha, *beta;
     double *lnl, *g_theta, *g_alpha, *g_beta;
     const oracle_fit_cfg* cfg; int32_t* iters; int32_t* status;
@@ -409,13 +409,13 @@ static void* batch_worker(void* arg) {
         pthread_mutex_unlock(&J->mu);
         if (w >= J->W) break;
         int64_t a = J->off[w], n = J->off[w + 1] - a;
-        const float* tw = J->t + a; const int32_t* mw = J->mark + a;
+        const double* tw = J->t + a; const int32_t* mw = J->mark + a;
         if (J->kind == 2) {
             J->status[w] = oracle_fit(J->D, n, tw, mw, J->T[w], J->cfg, J->theta + w * D,
                                       J->alpha + w * DD, J->beta + w * DD, J->lnl + w,
                                       J->iters + w, NULL);
         } else {
-            double (*ll)(int, int64_t, const float*, const int32_t*, double, const double*,
+            double (*ll)(int, int64_t, const double*, const int32_t*, double, const double*,
                          const double*, const double*, double*, double*, double*, double*) =
                 J->kind == 1 ? oracle_loglik_def : oracle_loglik_rec;
             J->lnl[w] = ll(J->D, n, tw, mw, J->T[w], J->theta + w * D, J->alpha + w * DD,
@@ -438,7 +438,7 @@ static void run_batch(batch_job* J, int nthreads) {
     pthread_mutex_destroy(&J->mu);
 }
 
-void oracle_loglik_batch(int use_def, int D, int64_t W, const float* t, const int32_t* mark,
+void oracle_loglik_batch(int use_def, int D, int64_t W, const double* t, const int32_t* mark,
                          const int64_t* win_off, const double* T, const double* theta,
                          const double* alpha, const double* beta, double* lnl,
                          double* g_theta, double* g_alpha, double* g_beta, int nthreads)
@@ -451,7 +451,7 @@ void oracle_loglik_batch(int use_def, int D, int64_t W, const float* t, const in
     run_batch(&J, nthreads);
 }
 
-void oracle_fit_batch(int D, int64_t W, const float* t, const int32_t* mark,
+void oracle_fit_batch(int D, int64_t W, const double* t, const int32_t* mark,
                       const int64_t* win_off, const double* T, const oracle_fit_cfg* cfg,
                       double* theta, double* alpha, double* beta, double* lnl,
                       int32_t* iters, int32_t* status, int nthreads)

@@ -18,6 +18,16 @@ int fit_launch(const Packed& P, const FitCfgDev& cfg, float* th, float* al, floa
                double* lnl, int32_t* iters, int32_t* status, float* trace, int* counter,
                cudaStream_t st);
 
+int seq_pack_launch(int D, int64_t N, int ce, double T, const double* t, const int32_t* mark,
+                    void* packed, int32_t* status_out, cudaStream_t st);
+int seq_loglik_launch(int D, int64_t N, int ce, double T, const void* pk, const float* th,
+                      const float* al, const float* be, double* lnl, float* gt, float* ga,
+                      float* gb, cudaStream_t st);
+int seq_fit_launch(int D, int64_t N, int ce, double T, const void* pk, const FitCfgDev& cfg,
+                   float* th, float* al, float* be, float* opt_state, double* lnl, int32_t* iters,
+                   int32_t* status, float* trace, cudaStream_t st);
+size_t seq_packed_bytes(int D, int64_t N, int ce);
+
 static thread_local char g_err[512] = "";
 static std::atomic<uint64_t> g_launches{0};
 
@@ -61,6 +71,39 @@ static int check_cuda(const char* what) {
     return MDHP_ECUDA;
   }
   return MDHP_OK;
+}
+
+static int check_seq(const mdhp_seq_desc* d) {
+  if (!d) {
+    set_error("desc is NULL");
+    return MDHP_EINVAL;
+  }
+  if (d->D < 1 || d->D > 32 || d->n_events < 0) {
+    set_error("bad sequence dims (D=%d, N=%lld)", d->D, (long long)d->n_events);
+    return MDHP_EDIM;
+  }
+  if (d->chunk_events < 8 || !(d->T > 0.0)) {
+    set_error("chunk_events must be >= 8 and T > 0");
+    return MDHP_EINVAL;
+  }
+  return MDHP_OK;
+}
+
+static FitCfgDev to_dev(const mdhp_fit_config* cfg) {
+  FitCfgDev c;
+  c.max_iters = cfg->max_iters;
+  c.optimizer = cfg->optimizer;
+  c.loss_mean = cfg->loss_mean;
+  c.patience = cfg->patience;
+  c.max_halvings = cfg->max_halvings;
+  c.lr = cfg->lr;
+  c.b1 = cfg->adam_b1;
+  c.b2 = cfg->adam_b2;
+  c.eps = cfg->adam_eps;
+  c.tol_rel = cfg->tol_rel;
+  c.min_param = cfg->min_param;
+  c.fit_mask = cfg->fit_mask;
+  return c;
 }
 
 static int check_cfg(const mdhp_fit_config* c) {
@@ -199,6 +242,76 @@ int mdhp_fit(const mdhp_pack_desc* d, const void* packed, const mdhp_fit_config*
   cudaFreeAsync(ws, st);
   if (rc) return rc;
   return check_cuda("mdhp_fit");
+}
+
+size_t mdhp_seq_packed_bytes(const mdhp_seq_desc* d) {
+  if (check_seq(d) != MDHP_OK) return 0;
+  return seq_packed_bytes(d->D, d->n_events, d->chunk_events);
+}
+
+int mdhp_seq_pack(const mdhp_seq_desc* d, const double* t, const int32_t* mark, void* packed,
+                  size_t packed_bytes, int32_t* status, void* stream) {
+  int rc = check_seq(d);
+  if (rc) return rc;
+  if (!packed || !status || (d->n_events > 0 && (!t || !mark))) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  const size_t need = seq_packed_bytes(d->D, d->n_events, d->chunk_events);
+  if (packed_bytes < need) {
+    set_error("packed buffer too small: %zu < %zu", packed_bytes, need);
+    return MDHP_ESIZE;
+  }
+  rc = seq_pack_launch(d->D, d->n_events, d->chunk_events, d->T, t, mark, packed, status,
+                       (cudaStream_t)stream);
+  if (rc) {
+    set_error("mdhp_seq_pack: CUDA error");
+    return rc;
+  }
+  return check_cuda("mdhp_seq_pack");
+}
+
+int mdhp_seq_loglik_grad(const mdhp_seq_desc* d, const void* packed, const float* theta,
+                         const float* alpha, const float* beta, double* loglik, float* g_theta,
+                         float* g_alpha, float* g_beta, void* stream) {
+  int rc = check_seq(d);
+  if (rc) return rc;
+  if (!packed || !theta || !alpha || !beta || !loglik) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  const bool any = g_theta || g_alpha || g_beta, all = g_theta && g_alpha && g_beta;
+  if (any && !all) {
+    set_error("g_theta, g_alpha, g_beta must be all NULL or all non-NULL");
+    return MDHP_EINVAL;
+  }
+  rc = seq_loglik_launch(d->D, d->n_events, d->chunk_events, d->T, packed, theta, alpha, beta,
+                         loglik, g_theta, g_alpha, g_beta, (cudaStream_t)stream);
+  if (rc) {
+    set_error("mdhp_seq_loglik_grad: CUDA error");
+    return rc;
+  }
+  return check_cuda("mdhp_seq_loglik_grad");
+}
+
+int mdhp_seq_fit(const mdhp_seq_desc* d, const void* packed, const mdhp_fit_config* cfg,
+                 float* theta, float* alpha, float* beta, float* opt_state, double* loglik,
+                 int32_t* iters, int32_t* status, float* lnl_trace, void* stream) {
+  int rc = check_seq(d);
+  if (rc) return rc;
+  rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (!packed || !theta || !alpha || !beta || !loglik || !iters || !status) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  rc = seq_fit_launch(d->D, d->n_events, d->chunk_events, d->T, packed, to_dev(cfg), theta, alpha,
+                      beta, opt_state, loglik, iters, status, lnl_trace, (cudaStream_t)stream);
+  if (rc) {
+    set_error("mdhp_seq_fit: CUDA error");
+    return rc;
+  }
+  return check_cuda("mdhp_seq_fit");
 }
 
 int mdhp_fit_host(const mdhp_pack_desc* d, const double* t_h, const int32_t* mark_h,

@@ -235,8 +235,11 @@ __device__ __forceinline__ void event_loop(const float2* __restrict__ A, float2*
                                            const float* __restrict__ dtp,
                                            const uint8_t* __restrict__ mk, const int64_t beg,
                                            const int n, const int nmax, const float th,
-                                           float& last, float& gth, double& lsum) {
-  last = -1.0f;
+                                           float& last, float& gth, double& lsum,
+                                           const float last0 = -1.0f) {
+  // last0: anchor of the initial state (-1: empty history; 0: a carried-in state anchored at
+  // the chunk base, seq.cu)
+  last = last0;
   gth = 0.0f;
   lsum = 0.0;
   Chunk c0, c1;

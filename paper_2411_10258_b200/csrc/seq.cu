@@ -1,0 +1,842 @@
+// seq.cu — long single sequences (row a7 of DESIGN.md section 4): chunked parallel scan of the
+// exponential-decay recurrence.
+//
+// The recurrence state of Eq.(2) for every pair (i, j) evolves between events as a
+// linear map: over a gap L, S <- e^{-beta L} S and Q <- e^{-beta L}(Q + L S), and an event of
+// source j adds 1 to S_.j.  So a long sequence can be cut into chunks (never inside a tie group):
+//   phase 1 (k_seq_local)  every chunk runs its column updates from a zero state -> its local
+//                          state at its last event (2 D^2 floats);
+//   phase 2 (k_seq_scan)   exclusive scan of the affine maps (decay over the chunk span + local
+//                          state), segmented over chunks, per pair -> the state carried into each
+//                          chunk, anchored at the chunk base (the previous chunk's last event);
+//   phase 3 (k_seq_eval)   every chunk re-runs the full event loop (row reads, lambda, gradient
+//                          accumulation) from its carried-in state;
+//   phase 4 (k_seq_reduce, k_seq_finish)  fixed-order sums over chunks, the Part2/Part3
+//                          epilogue from the global final state, and (fit) one optimizer step.
+// Chunk-relative fp32 times (fp64 base per chunk) keep ~1e-7 s resolution over 1000 s.
+#include <cmath>
+#include "eval.cuh"
+
+namespace mdhp {
+
+constexpr int kSeqWPB = 4;
+constexpr int kScanSeg = 64;
+
+struct SeqLayout {
+  int D, Dp;
+  int64_t N, C, Epad;
+  size_t cstart, cbeg, cspan, t32, dtp, mark, ccnt, cfirst, cmom, cnt, umax, mom, tail, status,
+      total;
+};
+
+__host__ __device__ inline SeqLayout make_seq_layout(int D, int64_t N, int ce) {
+  SeqLayout L;
+  L.D = D;
+  int p = 1;
+  while (p < D) p <<= 1;
+  L.Dp = p;
+  L.N = N;
+  L.C = N > 0 ? (N + ce - 1) / ce : 0;
+  L.Epad = ((N + 7) / 8) * 8 + 8 * L.C + 8;
+  size_t o = 0;
+  L.cstart = o; o = align256(o + sizeof(int64_t) * (L.C + 1));
+  L.cbeg = o;   o = align256(o + sizeof(int64_t) * L.C);
+  L.cspan = o;  o = align256(o + sizeof(float) * L.C);
+  L.t32 = o;    o = align256(o + sizeof(float) * L.Epad);
+  L.dtp = o;    o = align256(o + sizeof(float) * L.Epad);
+  L.mark = o;   o = align256(o + L.Epad);
+  L.ccnt = o;   o = align256(o + sizeof(int32_t) * L.C * L.Dp);
+  L.cfirst = o; o = align256(o + sizeof(double) * L.C * L.Dp);
+  L.cmom = o;   o = align256(o + sizeof(float) * L.C * L.Dp * kMom);
+  L.cnt = o;    o = align256(o + sizeof(int32_t) * L.Dp);
+  L.umax = o;   o = align256(o + sizeof(float) * L.Dp);
+  L.mom = o;    o = align256(o + sizeof(float) * L.Dp * kMom);
+  L.tail = o;   o = align256(o + sizeof(float) * 2);
+  L.status = o; o = align256(o + sizeof(int32_t));
+  L.total = o;
+  return L;
+}
+
+template <typename T>
+__host__ __device__ inline T* at(void* base, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(base) + off);
+}
+template <typename T>
+__host__ __device__ inline const T* at(const void* base, size_t off) {
+  return reinterpret_cast<const T*>(static_cast<const char*>(base) + off);
+}
+
+// ---------------------------------------------------------------- packing
+__global__ void k_seq_bounds(int64_t N, int64_t C, int ce, const double* __restrict__ t,
+                             int64_t* __restrict__ cstart, int64_t* __restrict__ cbeg) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > C) return;
+  int64_t b = c * ce;
+  if (b > N) b = N;
+  while (b > 0 && b < N && t[b] == t[b - 1]) b++;   // never split a tie group
+  cstart[c] = b;
+  if (c < C) cbeg[c] = ((b + 7) & ~int64_t(7)) + 8 * c;
+}
+
+// One warp per chunk: relative times, same-mark gaps, validation, per-chunk counts/first times.
+__global__ void __launch_bounds__(kSeqWPB * 32)
+k_seq_events(int D, int Dp, int64_t N, int64_t C, double T, const double* __restrict__ t,
+             const int32_t* __restrict__ mark, const int64_t* __restrict__ cstart,
+             const int64_t* __restrict__ cbeg, float* __restrict__ cspan, float* __restrict__ o_t,
+             float* __restrict__ o_d, uint8_t* __restrict__ o_m, int32_t* __restrict__ ccnt,
+             double* __restrict__ cfirst, int32_t* __restrict__ status) {
+  __shared__ double s_last[kSeqWPB][32];
+  __shared__ double s_first[kSeqWPB][32];
+  __shared__ int s_cnt[kSeqWPB][32];
+  const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * kSeqWPB + wp;
+  if (c >= C) return;
+  const int64_t a = cstart[c], z = cstart[c + 1], n = z - a, beg = cbeg[c];
+  const double tau = a > 0 ? t[a - 1] : 0.0;
+  s_last[wp][lane] = 0.0;
+  s_first[wp][lane] = 0.0;
+  s_cnt[wp][lane] = 0;
+  __syncwarp();
+  int st = 0;
+  double carry = tau;
+  for (int64_t base = 0; base < n; base += 32) {
+    const int64_t k = base + lane;
+    const bool in = k < n;
+    const double tk = in ? t[a + k] : 0.0;
+    const int mk = in ? mark[a + k] : 0;
+    const bool okmark = in && mk >= 0 && mk < D;
+    if (in) {
+      if (!isfinite(tk) || tk < 0.0 || tk > T) st |= MDHP_ST_OUT_OF_RANGE;
+      if (!okmark) st |= MDHP_ST_BAD_MARK;
+    }
+    double tprev = __shfl_up_sync(kFull, tk, 1);
+    if (lane == 0) tprev = carry;
+    if (in && tk < tprev) st |= MDHP_ST_UNSORTED;
+    carry = __shfl_sync(kFull, tk, 31);
+    const unsigned key = okmark ? (unsigned)mk : (64u + lane);
+    const unsigned grp = __match_any_sync(kFull, key);
+    const unsigned lower = grp & ((1u << lane) - 1u);
+    const int src = lower ? (31 - __clz(lower)) : lane;
+    const double tin = __shfl_sync(kFull, tk, src);
+    const int cnt_before = okmark ? s_cnt[wp][mk] : 0;
+    const bool has_prev = lower != 0 || cnt_before > 0;
+    const double tp = lower ? tin : (okmark && cnt_before > 0 ? s_last[wp][mk] : tau);
+    if (okmark && has_prev && tk == tp) st |= MDHP_ST_SAME_DIM_TIE;
+    if (in) {
+      o_t[beg + k] = __double2float_rn(__dsub_rn(tk, tau));
+      o_d[beg + k] = __double2float_rn(__dsub_rn(tk, tp));
+      o_m[beg + k] = okmark ? (uint8_t)mk : (uint8_t)0xFF;
+    }
+    if (okmark && !lower && cnt_before == 0) s_first[wp][mk] = tk;
+    __syncwarp();
+    const bool is_last = okmark && (grp & ~((2u << lane) - 1u)) == 0u;
+    if (is_last) {
+      s_last[wp][mk] = tk;
+      s_cnt[wp][mk] = cnt_before + __popc(grp);
+    }
+    __syncwarp();
+  }
+  const int64_t npad = (n + 7) & ~int64_t(7);
+  for (int64_t k = n + lane; k < npad; k += 32) {
+    o_t[beg + k] = kNullT;
+    o_d[beg + k] = 0.0f;
+    o_m[beg + k] = 0xFF;
+  }
+  if (lane < Dp) {
+    ccnt[c * Dp + lane] = lane < D ? s_cnt[wp][lane] : 0;
+    cfirst[c * Dp + lane] = s_first[wp][lane];
+  }
+  st = __reduce_or_sync(kFull, st);
+  if (lane == 0) {
+    cspan[c] = n > 0 ? __double2float_rn(__dsub_rn(t[z - 1], tau)) : 0.0f;
+    if (st) atomicOr(status, st);
+  }
+}
+
+// One warp: per-mark totals, first times -> u_max, and the tail T - (last event).
+__global__ void k_seq_stats(int D, int Dp, int64_t N, int64_t C, double T,
+                            const double* __restrict__ t, const int32_t* __restrict__ ccnt,
+                            const double* __restrict__ cfirst, int32_t* __restrict__ cnt,
+                            float* __restrict__ umax, float* __restrict__ tail,
+                            int32_t* __restrict__ status) {
+  const int j = threadIdx.x;
+  if (j < Dp) {
+    int tot = 0;
+    double first = 0.0;
+    bool have = false;
+    for (int64_t c = 0; c < C; c++) {
+      const int k = ccnt[c * Dp + j];
+      if (k > 0 && !have) {
+        first = cfirst[c * Dp + j];
+        have = true;
+      }
+      tot += k;
+    }
+    cnt[j] = j < D ? tot : 0;
+    umax[j] = (j < D && tot > 0) ? __double2float_rn(__dsub_rn(T, first)) : 0.0f;
+  }
+  if (j == 0) {
+    tail[0] = N > 0 ? __double2float_rn(__dsub_rn(T, t[N - 1])) : (float)T;
+    tail[1] = (float)T;
+    if (!(T > 0.0) || !isfinite(T)) atomicOr(status, MDHP_ST_BAD_T);
+    if (N == 0) atomicOr(status, MDHP_ST_EMPTY);
+  }
+}
+
+// Per-chunk power moments (lane = mark, fixed order), r = (T - t)/u_max in fp64.
+__global__ void __launch_bounds__(kSeqWPB * 32)
+k_seq_moments(int D, int Dp, int64_t C, double T, const double* __restrict__ t,
+              const int32_t* __restrict__ mark, const int64_t* __restrict__ cstart,
+              const float* __restrict__ umax, float* __restrict__ cmom) {
+  const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * kSeqWPB + wp;
+  if (c >= C) return;
+  const int64_t a = cstart[c], z = cstart[c + 1];
+  const double um = lane < D ? (double)umax[lane] : 0.0;
+  float acc[kMom];
+#pragma unroll
+  for (int p = 0; p < kMom; p++) acc[p] = 0.0f;
+  for (int64_t base = a; base < z; base += 32) {
+    const int64_t k = base + lane;
+    const double tk = k < z ? t[k] : 0.0;
+    const int mk = k < z ? mark[k] : -1;
+    const int cntk = (int)min((int64_t)32, z - base);
+    for (int s = 0; s < cntk; s++) {
+      const double ts = __shfl_sync(kFull, tk, s);
+      const int ms = __shfl_sync(kFull, mk, s);
+      if (ms == lane) {
+        const float r = um > 0.0 ? __double2float_rn((T - ts) / um) : 0.0f;
+        float pw = r;
+#pragma unroll
+        for (int p = 0; p < kMom; p++) {
+          acc[p] = __fadd_rn(acc[p], pw);
+          pw = __fmul_rn(pw, r);
+        }
+      }
+    }
+  }
+  if (lane < Dp) {
+#pragma unroll
+    for (int p = 0; p < kMom; p++) cmom[(c * Dp + lane) * kMom + p] = acc[p];
+  }
+}
+
+__global__ void k_seq_momsum(int Dp, int64_t C, const float* __restrict__ cmom,
+                             float* __restrict__ mom) {
+  const int q = threadIdx.x;   // (mark, p)
+  if (q >= Dp * kMom) return;
+  double s = 0.0;
+  for (int64_t c = 0; c < C; c++) s += (double)cmom[c * Dp * kMom + q];
+  mom[q] = (float)s;
+}
+
+// ---------------------------------------------------------------- evaluation workspace
+struct SeqWork {
+  float2* loc;     // [C][D*D]  local state at chunk end (target-major pairs)
+  float2* carry;   // [C][D*D]  state carried into the chunk, anchored at its base
+  float2* fin;     // [D*D]     state after the last event, anchored there
+  float2* gpart;   // [C][D*D]  per-chunk (gR, gQ)
+  float* gthp;     // [C][Dp]
+  double* lsp;     // [C]       per-chunk sum lg2 lambda
+  float2* gsum;    // [D*D]
+  float* gth;      // [Dp]
+  double* ls;      // [1]
+  int* ctl;        // optimizer control block (seq fit)
+  float* prev;     // [D + 2 D^2] previous point (rollback)
+  float* opt;      // [2 (D + 2 D^2)] Adam moments when the caller passes none
+  size_t bytes;
+};
+
+inline SeqWork make_seq_work(void* base, int D, int Dp, int64_t C) {
+  SeqWork w;
+  const size_t DD = (size_t)D * D, P = (size_t)D + 2 * DD;
+  size_t o = 0;
+  auto take = [&](size_t nb) { size_t r = o; o = align256(o + nb); return r; };
+  const size_t a = take(sizeof(float2) * C * DD), b = take(sizeof(float2) * C * DD),
+               f = take(sizeof(float2) * DD), g = take(sizeof(float2) * C * DD),
+               h = take(sizeof(float) * C * Dp), l = take(sizeof(double) * (C + 1)),
+               gs = take(sizeof(float2) * DD), gt = take(sizeof(float) * Dp), ls = take(sizeof(double)),
+               ct = take(sizeof(int) * 64), pv = take(sizeof(float) * P), op = take(sizeof(float) * 2 * P);
+  char* B = static_cast<char*>(base);
+  w.loc = reinterpret_cast<float2*>(B + a);
+  w.carry = reinterpret_cast<float2*>(B + b);
+  w.fin = reinterpret_cast<float2*>(B + f);
+  w.gpart = reinterpret_cast<float2*>(B + g);
+  w.gthp = reinterpret_cast<float*>(B + h);
+  w.lsp = reinterpret_cast<double*>(B + l);
+  w.gsum = reinterpret_cast<float2*>(B + gs);
+  w.gth = reinterpret_cast<float*>(B + gt);
+  w.ls = reinterpret_cast<double*>(B + ls);
+  w.ctl = reinterpret_cast<int*>(B + ct);
+  w.prev = reinterpret_cast<float*>(B + pv);
+  w.opt = reinterpret_cast<float*>(B + op);
+  w.bytes = o;
+  return w;
+}
+
+// optimizer control block (device), one sequence
+struct SeqCtl {
+  int done, it, s, halv, stall, st, have_prev, have_lnl;
+  float lr_w;
+  int pad;
+  double lnl_prev, lnl_last;
+};
+
+// Phase 1: column updates only, from a zero state; local state converted to the chunk end.
+template <int DP>
+__global__ void __launch_bounds__(128)
+k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* __restrict__ cbeg,
+            const float* __restrict__ cspan, const float* __restrict__ t32,
+            const float* __restrict__ dtp, const uint8_t* __restrict__ mk,
+            const float* __restrict__ beta, float2* __restrict__ loc, const int* __restrict__ ctl) {
+  if (ctl && ctl[0]) return;
+  constexpr int G = 32 / DP, RS = DP + 1;
+  extern __shared__ __align__(16) unsigned char smem_l[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / DP, j = lane % DP;
+  const int gbase = g * DP;
+  float2* SQ = reinterpret_cast<float2*>(smem_l) + (size_t)(wid * G + g) * DP * RS;
+  float* B = reinterpret_cast<float*>(reinterpret_cast<float2*>(smem_l) + (size_t)4 * G * DP * RS) +
+             (size_t)(wid * G + g) * DP * RS;
+  const int64_t c = ((int64_t)blockIdx.x * 4 + wid) * G + g;
+  const bool live = c < C;
+  const int n = live ? (int)(cstart[c + 1] - cstart[c]) : 0;
+  for (int i = 0; i < DP; i++) {
+    SQ[j * RS + i] = make_float2(0.0f, 0.0f);
+    B[j * RS + i] = (j < D && i < D) ? beta[(size_t)j * D + i] : 0.0f;   // beta_ji: row j, col i
+  }
+  __syncwarp();
+  int nmax = n;
+  for (int o = 16; o >= 1; o >>= 1) nmax = max(nmax, __shfl_xor_sync(kFull, nmax, o));
+  const int64_t beg = live ? cbeg[c] : 0;
+  float last = -1.0f;
+  for (int k = 0; k < nmax; k++) {
+    const bool act = k < n;
+    const float t = act ? t32[beg + k] : 0.0f;
+    const float dc = act ? dtp[beg + k] : 0.0f;
+    const int i = act ? (int)mk[beg + k] : 0;
+    if (act) {
+      const float2 s = SQ[j * RS + i];
+      const float e = ex2f(B[j * RS + i] * (dc * -kLog2e));
+      SQ[j * RS + i] = make_float2(fmaf(e, s.x, 1.0f), e * fmaf(dc, s.x, s.y));
+      if (i == j) last = t;
+    }
+    __syncwarp();
+  }
+  const float Lc = live ? cspan[c] : 0.0f;
+  for (int i = 0; i < DP; i++) {
+    const float li = __shfl_sync(kFull, last, gbase + i);
+    if (live && j < D && i < D) {
+      float2 s = SQ[j * RS + i];
+      if (li >= 0.0f) {
+        const float dl = Lc - li;
+        const float e = ex2f(B[j * RS + i] * (dl * -kLog2e));
+        s = make_float2(e * s.x, e * fmaf(dl, s.x, s.y));
+      } else {
+        s = make_float2(0.0f, 0.0f);
+      }
+      loc[(size_t)c * D * D + (size_t)j * D + i] = s;
+    }
+  }
+}
+
+// Phase 2: exclusive scan of the per-chunk affine maps, one block per pair, kScanSeg segments.
+__global__ void __launch_bounds__(kScanSeg)
+k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __restrict__ beta,
+           const float2* __restrict__ loc, float2* __restrict__ carry, float2* __restrict__ fin,
+           const int* __restrict__ ctl) {
+  if (ctl && ctl[0]) return;
+  __shared__ float2 sx[kScanSeg];
+  __shared__ float sl[kScanSeg];
+  __shared__ float2 sc[kScanSeg + 1];
+  const int p = blockIdx.x, s = threadIdx.x;
+  const size_t DD = (size_t)D * D;
+  const float b = beta[p];
+  const int64_t per = (C + kScanSeg - 1) / kScanSeg;
+  const int64_t c0 = min(C, (int64_t)s * per), c1 = min(C, c0 + per);
+  auto step = [&](float2 x, float L, float2 l) {
+    const float e = ex2f(b * (L * -kLog2e));
+    return make_float2(fmaf(e, x.x, l.x), fmaf(e, fmaf(L, x.x, x.y), l.y));
+  };
+  float2 x = make_float2(0.0f, 0.0f);
+  float Ls = 0.0f;
+  for (int64_t c = c0; c < c1; c++) {
+    x = step(x, cspan[c], loc[c * DD + p]);
+    Ls += cspan[c];
+  }
+  sx[s] = x;
+  sl[s] = Ls;
+  __syncthreads();
+  if (s == 0) {
+    float2 y = make_float2(0.0f, 0.0f);
+    for (int q = 0; q < kScanSeg; q++) {
+      sc[q] = y;
+      y = step(y, sl[q], sx[q]);
+    }
+    sc[kScanSeg] = y;
+    fin[p] = y;
+  }
+  __syncthreads();
+  x = sc[s];
+  for (int64_t c = c0; c < c1; c++) {
+    carry[c * DD + p] = x;
+    x = step(x, cspan[c], loc[c * DD + p]);
+  }
+}
+
+// Phase 3: full event loop per chunk from its carried-in state; per-chunk partial sums.
+template <int DP>
+__global__ void __launch_bounds__(128)
+k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* __restrict__ cbeg,
+           const float* __restrict__ t32, const float* __restrict__ dtp,
+           const uint8_t* __restrict__ mk, const float* __restrict__ theta,
+           const float* __restrict__ alpha, const float* __restrict__ beta,
+           const float2* __restrict__ carry, float2* __restrict__ gpart, float* __restrict__ gthp,
+           double* __restrict__ lsp, int grad, const int* __restrict__ ctl) {
+  if (ctl && ctl[0] == 1 && grad) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  using SM = Smem<DP>;
+  constexpr int RS = DP + 1;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / DP, j = lane % DP;
+  const int gbase = g * DP;
+  float2* base = reinterpret_cast<float2*>(smem + wid * SM::per_warp) + g * SM::per_group;
+  float2* A = base;
+  float2* SQ = base + SM::AS;
+  float2* Gs = base + 2 * SM::AS;
+  const int64_t c = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wid) * SM::G + g;
+  const bool live = c < C;
+  const size_t DD = (size_t)D * D;
+  for (int i = 0; i < DP; i++) {
+    const bool real = live && i < D && j < D;
+    A[i * RS + j] = real ? make_float2(alpha[(size_t)i * D + j], beta[(size_t)i * D + j])
+                         : make_float2(0.0f, 1.0f);
+    SQ[i * RS + j] = real ? carry[(size_t)c * DD + (size_t)i * D + j] : make_float2(0.0f, 0.0f);
+    Gs[i * DP + j] = make_float2(0.0f, 0.0f);
+  }
+  A[DP * RS + j] = make_float2(j == 0 ? 1.0f : 0.0f, 0.0f);
+  A[j * RS + DP] = make_float2(0.0f, 0.0f);
+  SQ[DP * RS + j] = make_float2(j == 0 ? 1.0f : 0.0f, 0.0f);
+  SQ[j * RS + DP] = make_float2(0.0f, 0.0f);
+  const float th = (live && j < D) ? theta[j] : 0.0f;
+  __syncwarp();
+  const int n = live ? (int)(cstart[c + 1] - cstart[c]) : 0;
+  int nmax = n;
+  for (int o = 16; o >= 1; o >>= 1) nmax = max(nmax, __shfl_xor_sync(kFull, nmax, o));
+  float last, gth;
+  double lsum;
+  // chunk 0 starts from an empty history (anchor -1, as a window); later chunks from a state
+  // anchored at their base (relative time 0; their events are strictly later, R2/R10)
+  const float last0 = c == 0 ? -1.0f : 0.0f;
+  if (grad)
+    event_loop<DP, true>(A, SQ, Gs, j, gbase, t32, dtp, mk, live ? cbeg[c] : 0, n, nmax, th, last,
+                         gth, lsum, last0);
+  else
+    event_loop<DP, false>(A, SQ, Gs, j, gbase, t32, dtp, mk, live ? cbeg[c] : 0, n, nmax, th,
+                          last, gth, lsum, last0);
+  lsum = group_sum_d<DP>(lsum);
+  if (!live) return;
+  if (j == 0) lsp[c] = lsum;
+  if (grad) {
+    if (j < D) gthp[c * DP + j] = gth;
+    for (int i = 0; i < D; i++)
+      if (j < D) gpart[(size_t)c * DD + (size_t)i * D + j] = Gs[i * DP + j];
+  }
+}
+
+// Phase 4a: fixed-order sums over chunks.  Blocks 0..D^2-1: pair p; block D^2: g_theta, lsum.
+__global__ void __launch_bounds__(256)
+k_seq_reduce(int D, int Dp, int64_t C, const float2* __restrict__ gpart,
+             const float* __restrict__ gthp, const double* __restrict__ lsp,
+             float2* __restrict__ gsum, float* __restrict__ gth, double* __restrict__ ls,
+             int grad, const int* __restrict__ ctl) {
+  if (ctl && ctl[0] == 1 && grad) return;
+  __shared__ double sa[256], sbv[256];
+  const int tid = threadIdx.x;
+  const size_t DD = (size_t)D * D;
+  const int p = blockIdx.x;
+  double a = 0.0, b = 0.0;
+  if (p < (int)DD) {
+    if (!grad) return;
+    for (int64_t c = tid; c < C; c += 256) {
+      const float2 v = gpart[c * DD + p];
+      a += v.x;
+      b += v.y;
+    }
+  } else {
+    for (int64_t c = tid; c < C; c += 256) a += lsp[c];
+  }
+  sa[tid] = a;
+  sbv[tid] = b;
+  __syncthreads();
+  for (int o = 128; o >= 1; o >>= 1) {
+    if (tid < o) {
+      sa[tid] += sa[tid + o];
+      sbv[tid] += sbv[tid + o];
+    }
+    __syncthreads();
+  }
+  if (p < (int)DD) {
+    if (tid == 0) gsum[p] = make_float2((float)sa[0], (float)sbv[0]);
+  } else {
+    if (tid == 0) ls[0] = sa[0];
+    if (grad && tid < D) {
+      double s = 0.0;
+      for (int64_t c = 0; c < C; c++) s += gthp[c * Dp + tid];
+      gth[tid] = (float)s;
+    }
+  }
+}
+
+// Fit gate: an invalid sequence is not fitted; its validation bits go to the caller's status.
+__global__ void k_seq_gate(const int32_t* __restrict__ pst, int* __restrict__ ctl,
+                           int32_t* __restrict__ status) {
+  const int s = pst[0];
+  status[0] = s;
+  if (s & MDHP_ST_INVALID) ctl[0] = 1;
+}
+
+// Phase 4b: epilogue (+ optional optimizer step for the sequence fit).  One block of D^2
+// threads (thread = pair (i, j), target-major).
+__global__ void __launch_bounds__(1024)
+k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
+             const int32_t* __restrict__ cnt, const float* __restrict__ umax,
+             const float* __restrict__ mom, const float2* __restrict__ fin,
+             const float2* __restrict__ gsum, const float* __restrict__ gthv,
+             const double* __restrict__ ls, float* __restrict__ theta, float* __restrict__ alpha,
+             float* __restrict__ beta, double* __restrict__ lnl_out, float* __restrict__ g_theta,
+             float* __restrict__ g_alpha, float* __restrict__ g_beta, int grad,
+             // fit-only arguments (ctl == nullptr: plain evaluation)
+             int* __restrict__ ctl_i, FitCfgDev cfg, float* __restrict__ prev,
+             float* __restrict__ opt, float* __restrict__ trace, int64_t n_events,
+             int32_t* __restrict__ status_out, int32_t* __restrict__ iters_out,
+             const int32_t* __restrict__ pstatus) {
+  const bool invalid = (pstatus[0] & MDHP_ST_INVALID) != 0;
+  SeqCtl* ctl = reinterpret_cast<SeqCtl*>(ctl_i);
+  if (ctl && ctl->done && grad) return;
+  __shared__ double red[1024];
+  __shared__ int okflag;
+  __shared__ double s_lnl;
+  const int tid = threadIdx.x;
+  const int DD = D * D;
+  const int i = tid / D, j = tid % D;
+  const bool pair = tid < DD;
+  if (tid == 0) okflag = 1;
+  __syncthreads();
+  double part3 = 0.0;
+  float da = 0.0f, db = 0.0f;
+  if (pair) {
+    ColInfo ci;
+    ci.real = true;
+    ci.T = tail[0];       // T - (last event): the final state is anchored at the last event
+    ci.last = 0.0f;
+    ci.N = cnt[j];
+    ci.umax = umax[j];
+    Series S;
+    load_series(S, mom + (size_t)j * kMom, ci.N > 0);
+    const float a = alpha[tid], b = beta[tid];
+    const float2 f = fin[tid];
+    float Eb, Hb2;
+    compensator(ci, S, b, f.x, f.y, Eb, Hb2);
+    part3 = (double)(a * Eb);
+    if (grad) {
+      const float2 gg = gsum[tid];
+      da = gg.x + Eb;
+      db = fmaf(-a, gg.y, a * Hb2);
+      if (!isfinite(da) || !isfinite(db)) okflag = 0;
+    }
+  }
+  double sth = (tid < D) ? (double)theta[tid] : 0.0;
+  float dth = 0.0f;
+  if (grad && tid < D) {
+    dth = gthv[tid] - (float)T;
+    if (!isfinite(dth)) okflag = 0;
+  }
+  red[tid] = part3;
+  __syncthreads();
+  for (int o = 512; o >= 1; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  const double p3 = red[0];
+  __syncthreads();
+  red[tid] = sth;
+  __syncthreads();
+  for (int o = 512; o >= 1; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  const double lnl = (double)kLn2 * ls[0] + p3 - T * red[0];
+  if (!ctl) {
+    if (tid == 0) lnl_out[0] = invalid ? (double)NAN : lnl;
+    if (grad) {
+      if (tid < D) g_theta[tid] = invalid ? NAN : dth;
+      if (pair) {
+        g_alpha[tid] = invalid ? NAN : da;
+        g_beta[tid] = invalid ? NAN : db;
+      }
+    }
+    return;
+  }
+  // ---- sequence fit: one iteration of the loop of DESIGN.md "Fit" (same as k_fit)
+  if (!grad) {   // final evaluation at the returned point
+    if (tid == 0) {
+      lnl_out[0] = invalid ? (double)NAN : lnl;
+      iters_out[0] = ctl->it;
+      status_out[0] |= ctl->st;
+    }
+    return;
+  }
+  const size_t P = (size_t)D + 2 * (size_t)DD;
+  const bool finite = okflag && isfinite(lnl);
+  __shared__ int act;   // 0 = stop, 1 = step, 2 = rollback
+  if (tid == 0) {
+    act = 0;
+    if (!finite) {
+      ctl->st |= MDHP_ST_NONFINITE;
+      if (!ctl->have_prev || ctl->halv >= cfg.max_halvings) {
+        ctl->st |= MDHP_ST_DIVERGED;
+        ctl->done = 1;
+        act = ctl->have_prev ? 2 : 0;
+      } else {
+        ctl->lr_w *= 0.5f;
+        ctl->halv++;
+        ctl->it++;
+        act = 2;
+      }
+    } else {
+      if (trace) trace[ctl->it] = (float)lnl;
+      bool stop = false;
+      if (cfg.tol_rel > 0.0f && ctl->have_lnl) {
+        const double thr = (double)cfg.tol_rel * fmax(fabs(ctl->lnl_prev), 1.0);
+        ctl->stall = (fabs(lnl - ctl->lnl_prev) <= thr) ? ctl->stall + 1 : 0;
+        if (ctl->stall >= cfg.patience) {
+          ctl->st |= MDHP_ST_CONVERGED;
+          ctl->done = 1;
+          stop = true;
+        }
+      }
+      if (!stop) {
+        ctl->lnl_prev = lnl;
+        ctl->have_lnl = 1;
+        ctl->have_prev = 1;
+        ctl->s++;
+        act = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (act == 2) {   // roll back to the previous point
+    if (tid < D) theta[tid] = prev[tid];
+    if (pair) {
+      alpha[tid] = prev[D + tid];
+      beta[tid] = prev[D + DD + tid];
+    }
+  } else if (act == 1) {
+    // save the previous point, then step
+    if (tid < D) prev[tid] = theta[tid];
+    if (pair) {
+      prev[D + tid] = alpha[tid];
+      prev[D + DD + tid] = beta[tid];
+    }
+    const float lr_w = ctl->lr_w;
+    const int s = ctl->s;
+    const float scale = (cfg.loss_mean && n_events > 0) ? 1.0f / (float)n_events : 1.0f;
+    const bool adam = cfg.optimizer == MDHP_OPT_ADAM;
+    const float bc1 = adam ? 1.0f - powf(cfg.b1, (float)s) : 1.0f;
+    const float sbc2 = adam ? sqrtf(1.0f - powf(cfg.b2, (float)s)) : 1.0f;
+    auto upd = [&](float p, float g, size_t q, float lo) -> float {
+      const float gl = -g * scale;
+      if (adam) {
+        const float mm = cfg.b1 * opt[q] + (1.0f - cfg.b1) * gl;
+        const float vv = cfg.b2 * opt[P + q] + (1.0f - cfg.b2) * gl * gl;
+        opt[q] = mm;
+        opt[P + q] = vv;
+        p = p - (lr_w / bc1) * (mm / (sqrtf(vv) / sbc2 + cfg.eps));
+      } else {
+        p = p - lr_w * gl;
+      }
+      return p < lo ? lo : p;
+    };
+    if (tid < D && (cfg.fit_mask & MDHP_FIT_THETA)) theta[tid] = upd(theta[tid], dth, tid, cfg.min_param);
+    if (pair) {
+      if (cfg.fit_mask & MDHP_FIT_ALPHA) alpha[tid] = upd(alpha[tid], da, D + tid, 0.0f);
+      if (cfg.fit_mask & MDHP_FIT_BETA) beta[tid] = upd(beta[tid], db, D + DD + tid, cfg.min_param);
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && act == 1) {
+    ctl->it++;
+  }
+  __syncthreads();
+  if (tid == 0 && ctl->it >= cfg.max_iters) ctl->done = 1;
+}
+
+// ---------------------------------------------------------------- host side
+int seq_pack_launch(int D, int64_t N, int ce, double T, const double* t, const int32_t* mark,
+                    void* packed, int32_t* status_out, cudaStream_t st) {
+  const SeqLayout L = make_seq_layout(D, N, ce);
+  if (cudaMemsetAsync(at<int32_t>(packed, L.status), 0, sizeof(int32_t), st) != cudaSuccess)
+    return MDHP_ECUDA;
+  const int64_t C = L.C;
+  if (C > 0) {
+    k_seq_bounds<<<(unsigned)((C + 1 + 255) / 256), 256, 0, st>>>(
+        N, C, ce, t, at<int64_t>(packed, L.cstart), at<int64_t>(packed, L.cbeg));
+    const unsigned blocks = (unsigned)((C + kSeqWPB - 1) / kSeqWPB);
+    k_seq_events<<<blocks, kSeqWPB * 32, 0, st>>>(
+        D, L.Dp, N, C, T, t, mark, at<int64_t>(packed, L.cstart), at<int64_t>(packed, L.cbeg),
+        at<float>(packed, L.cspan), at<float>(packed, L.t32), at<float>(packed, L.dtp),
+        at<uint8_t>(packed, L.mark), at<int32_t>(packed, L.ccnt), at<double>(packed, L.cfirst),
+        at<int32_t>(packed, L.status));
+    count_launch(2);
+  }
+  k_seq_stats<<<1, 32, 0, st>>>(D, L.Dp, N, C, T, t, at<int32_t>(packed, L.ccnt),
+                                at<double>(packed, L.cfirst), at<int32_t>(packed, L.cnt),
+                                at<float>(packed, L.umax), at<float>(packed, L.tail),
+                                at<int32_t>(packed, L.status));
+  count_launch(1);
+  if (C > 0) {
+    k_seq_moments<<<(unsigned)((C + kSeqWPB - 1) / kSeqWPB), kSeqWPB * 32, 0, st>>>(
+        D, L.Dp, C, T, t, mark, at<int64_t>(packed, L.cstart), at<float>(packed, L.umax),
+        at<float>(packed, L.cmom));
+    count_launch(1);
+  }
+  if (cudaMemsetAsync(at<float>(packed, L.mom), 0, sizeof(float) * L.Dp * kMom, st) != cudaSuccess)
+    return MDHP_ECUDA;
+  if (C > 0) {
+    k_seq_momsum<<<1, ((L.Dp * kMom + 31) / 32) * 32, 0, st>>>(L.Dp, C, at<float>(packed, L.cmom),
+                                                               at<float>(packed, L.mom));
+    count_launch(1);
+  }
+  if (status_out &&
+      cudaMemcpyAsync(status_out, at<int32_t>(packed, L.status), sizeof(int32_t),
+                      cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return MDHP_ECUDA;
+  return cudaGetLastError() == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
+}
+
+template <int DP>
+static void seq_phases_t(const SeqLayout& L, const void* pk, const float* th, const float* al,
+                         const float* be, const SeqWork& w, int grad, const int* ctl,
+                         cudaStream_t st) {
+  const int64_t C = L.C;
+  if (C == 0) return;
+  constexpr int G = 32 / DP;
+  const unsigned blk = (unsigned)((C + 4 * G - 1) / (4 * G));
+  const size_t lsm = (size_t)4 * G * DP * (DP + 1) * (sizeof(float2) + sizeof(float));
+  cudaFuncSetAttribute(k_seq_local<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
+  k_seq_local<DP><<<blk, 128, lsm, st>>>(L.D, C, at<int64_t>(pk, L.cstart), at<int64_t>(pk, L.cbeg),
+                                       at<float>(pk, L.cspan), at<float>(pk, L.t32),
+                                       at<float>(pk, L.dtp), at<uint8_t>(pk, L.mark), be, w.loc,
+                                       grad ? ctl : nullptr);
+  k_seq_scan<<<L.D * L.D, kScanSeg, 0, st>>>(L.D, C, at<float>(pk, L.cspan), be, w.loc, w.carry,
+                                             w.fin, grad ? ctl : nullptr);
+  using SM = Smem<DP>;
+  const size_t smem = 4 * SM::per_warp;
+  cudaFuncSetAttribute(k_seq_eval<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_seq_eval<DP><<<blk, 128, smem, st>>>(L.D, C, at<int64_t>(pk, L.cstart), at<int64_t>(pk, L.cbeg),
+                                         at<float>(pk, L.t32), at<float>(pk, L.dtp),
+                                         at<uint8_t>(pk, L.mark), th, al, be, w.carry, w.gpart,
+                                         w.gthp, w.lsp, grad, ctl);
+  count_launch(3);
+}
+
+static void seq_phases(const SeqLayout& L, const void* pk, const float* th, const float* al,
+                       const float* be, const SeqWork& w, int grad, const int* ctl,
+                       cudaStream_t st) {
+  switch (L.Dp) {
+    case 1: seq_phases_t<1>(L, pk, th, al, be, w, grad, ctl, st); break;
+    case 2: seq_phases_t<2>(L, pk, th, al, be, w, grad, ctl, st); break;
+    case 4: seq_phases_t<4>(L, pk, th, al, be, w, grad, ctl, st); break;
+    case 8: seq_phases_t<8>(L, pk, th, al, be, w, grad, ctl, st); break;
+    case 16: seq_phases_t<16>(L, pk, th, al, be, w, grad, ctl, st); break;
+    case 32: seq_phases_t<32>(L, pk, th, al, be, w, grad, ctl, st); break;
+  }
+}
+
+static void seq_reduce(const SeqLayout& L, const SeqWork& w, int grad, const int* ctl,
+                       cudaStream_t st) {
+  if (L.C == 0) return;
+  k_seq_reduce<<<L.D * L.D + 1, 256, 0, st>>>(L.D, L.Dp, L.C, w.gpart, w.gthp, w.lsp, w.gsum,
+                                               w.gth, w.ls, grad, ctl);
+  count_launch(1);
+}
+
+static size_t seq_work_bytes(const SeqLayout& L) {
+  return make_seq_work(nullptr, L.D, L.Dp, L.C).bytes;
+}
+
+// zero-sized sequences: fin/gsum/gth/ls must read as zero
+static int seq_work_init(const SeqLayout& L, void* ws, size_t bytes, cudaStream_t st) {
+  return cudaMemsetAsync(ws, 0, bytes, st) == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
+}
+
+int seq_loglik_launch(int D, int64_t N, int ce, double T, const void* pk, const float* th,
+                      const float* al, const float* be, double* lnl, float* gt, float* ga,
+                      float* gb, cudaStream_t st) {
+  const SeqLayout L = make_seq_layout(D, N, ce);
+  const size_t wb = seq_work_bytes(L);
+  void* ws = nullptr;
+  if (cudaMallocAsync(&ws, wb, st) != cudaSuccess) return MDHP_ECUDA;
+  int rc = seq_work_init(L, ws, wb, st);
+  const SeqWork w = make_seq_work(ws, D, L.Dp, L.C);
+  const int grad = gt != nullptr;
+  seq_phases(L, pk, th, al, be, w, grad, nullptr, st);
+  seq_reduce(L, w, grad, nullptr, st);
+  FitCfgDev cfg{};
+  k_seq_finish<<<1, 1024, 0, st>>>(D, L.Dp, T, at<float>(pk, L.tail), at<int32_t>(pk, L.cnt),
+                                   at<float>(pk, L.umax), at<float>(pk, L.mom), w.fin, w.gsum,
+                                   w.gth, w.ls, const_cast<float*>(th), const_cast<float*>(al),
+                                   const_cast<float*>(be), lnl, gt, ga, gb, grad, nullptr, cfg,
+                                   nullptr, nullptr, nullptr, N, nullptr, nullptr,
+                                   at<int32_t>(pk, L.status));
+  count_launch(1);
+  cudaFreeAsync(ws, st);
+  if (cudaGetLastError() != cudaSuccess) rc = MDHP_ECUDA;
+  return rc;
+}
+
+int seq_fit_launch(int D, int64_t N, int ce, double T, const void* pk, const FitCfgDev& cfg,
+                   float* th, float* al, float* be, float* opt_state, double* lnl, int32_t* iters,
+                   int32_t* status, float* trace, cudaStream_t st) {
+  const SeqLayout L = make_seq_layout(D, N, ce);
+  const size_t wb = seq_work_bytes(L);
+  void* ws = nullptr;
+  if (cudaMallocAsync(&ws, wb, st) != cudaSuccess) return MDHP_ECUDA;
+  int rc = seq_work_init(L, ws, wb, st);
+  const SeqWork w = make_seq_work(ws, D, L.Dp, L.C);
+  float* opt = opt_state ? opt_state : w.opt;
+  // control block: done = (invalid input or max_iters == 0), lr_w = lr
+  SeqCtl h{};
+  h.lr_w = cfg.lr;
+  h.done = cfg.max_iters <= 0;
+  cudaMemcpyAsync(w.ctl, &h, sizeof(SeqCtl), cudaMemcpyHostToDevice, st);
+  // an invalid sequence (validation bits) is not fitted
+  k_seq_gate<<<1, 1, 0, st>>>(at<const int32_t>(pk, L.status), w.ctl, status);
+  count_launch(1);
+  if (trace) cudaMemsetAsync(trace, 0xff, sizeof(float) * (size_t)(cfg.max_iters > 0 ? cfg.max_iters : 1), st);
+  for (int it = 0; it < cfg.max_iters; it++) {
+    seq_phases(L, pk, th, al, be, w, 1, w.ctl, st);
+    seq_reduce(L, w, 1, w.ctl, st);
+    k_seq_finish<<<1, 1024, 0, st>>>(D, L.Dp, T, at<float>(pk, L.tail), at<int32_t>(pk, L.cnt),
+                                     at<float>(pk, L.umax), at<float>(pk, L.mom), w.fin, w.gsum,
+                                     w.gth, w.ls, th, al, be, lnl, nullptr, nullptr, nullptr, 1,
+                                     w.ctl, cfg, w.prev, opt, trace, N, status, iters,
+                                     at<int32_t>(pk, L.status));
+    count_launch(1);
+  }
+  // lnL at the returned point
+  seq_phases(L, pk, th, al, be, w, 0, nullptr, st);
+  seq_reduce(L, w, 0, nullptr, st);
+  k_seq_finish<<<1, 1024, 0, st>>>(D, L.Dp, T, at<float>(pk, L.tail), at<int32_t>(pk, L.cnt),
+                                   at<float>(pk, L.umax), at<float>(pk, L.mom), w.fin, w.gsum,
+                                   w.gth, w.ls, th, al, be, lnl, nullptr, nullptr, nullptr, 0,
+                                   w.ctl, cfg, w.prev, opt, trace, N, status, iters,
+                                   at<int32_t>(pk, L.status));
+  count_launch(1);
+  cudaFreeAsync(ws, st);
+  if (cudaGetLastError() != cudaSuccess) rc = MDHP_ECUDA;
+  return rc;
+}
+
+size_t seq_packed_bytes(int D, int64_t N, int ce) { return make_seq_layout(D, N, ce).total; }
+
+}  // namespace mdhp

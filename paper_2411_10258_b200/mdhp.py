@@ -29,6 +29,11 @@ class PackDesc(ctypes.Structure):
                 ("eq6_lo", ctypes.c_double), ("eq6_hi", ctypes.c_double)]
 
 
+class SeqDesc(ctypes.Structure):
+    _fields_ = [("D", ctypes.c_int32), ("chunk_events", ctypes.c_int32),
+                ("n_events", ctypes.c_int64), ("T", ctypes.c_double)]
+
+
 class FitConfigC(ctypes.Structure):
     _fields_ = [("max_iters", ctypes.c_int32), ("optimizer", ctypes.c_int32),
                 ("lr", ctypes.c_float), ("adam_b1", ctypes.c_float), ("adam_b2", ctypes.c_float),
@@ -86,6 +91,15 @@ def lib() -> ctypes.CDLL:
         L.mdhp_fit_host.restype = ctypes.c_int
         L.mdhp_fit_host.argtypes = [ctypes.POINTER(PackDesc), P, P, P, P, ctypes.POINTER(FitConfigC),
                                     P, P, P, P, P, P, P]
+        L.mdhp_seq_packed_bytes.restype = ctypes.c_size_t
+        L.mdhp_seq_packed_bytes.argtypes = [ctypes.POINTER(SeqDesc)]
+        L.mdhp_seq_pack.restype = ctypes.c_int
+        L.mdhp_seq_pack.argtypes = [ctypes.POINTER(SeqDesc), P, P, P, ctypes.c_size_t, P, P]
+        L.mdhp_seq_loglik_grad.restype = ctypes.c_int
+        L.mdhp_seq_loglik_grad.argtypes = [ctypes.POINTER(SeqDesc), P, P, P, P, P, P, P, P, P]
+        L.mdhp_seq_fit.restype = ctypes.c_int
+        L.mdhp_seq_fit.argtypes = [ctypes.POINTER(SeqDesc), P, ctypes.POINTER(FitConfigC), P, P, P, P, P,
+                                   P, P, P, P]
         L.mdhp_packed_layout.restype = ctypes.c_int
         L.mdhp_packed_layout.argtypes = [ctypes.POINTER(PackDesc), P]
         L.mdhp_last_error.restype = ctypes.c_char_p
@@ -255,3 +269,65 @@ def fit_host(D, t, mark, win_off, T, theta, alpha, beta, cfg: FitConfig, time_mo
                              _ptr(iters), _ptr(status), _stream(stream))
     _check(rc, "mdhp_fit_host")
     return {"lnl": lnl, "iters": iters, "status": status}
+
+
+# ------------------------------------------------------------------ long single sequences (a7)
+@dataclass
+class PackedSeq:
+    desc: SeqDesc
+    buf: torch.Tensor
+    status: torch.Tensor   # int32 [1] device
+
+    @property
+    def D(self):
+        return int(self.desc.D)
+
+
+def seq_pack(D, t, mark, T, chunk_events=256, out: PackedSeq | None = None, stream=None) -> PackedSeq:
+    """mdhp_seq_pack on CUDA tensors t f64[N], mark i32[N] (one sequence on [0, T])."""
+    _dev(t, torch.float64, "t"); _dev(mark, torch.int32, "mark")
+    desc = SeqDesc(int(D), int(chunk_events), int(t.numel()), float(T))
+    nb = int(lib().mdhp_seq_packed_bytes(ctypes.byref(desc)))
+    if nb == 0:
+        _check(-2, "mdhp_seq_packed_bytes")
+    if out is None or out.buf.numel() < nb:
+        buf = torch.empty(nb, dtype=torch.uint8, device=t.device)
+        status = torch.zeros(1, dtype=torch.int32, device=t.device)
+    else:
+        buf, status = out.buf, out.status
+    rc = lib().mdhp_seq_pack(ctypes.byref(desc), _ptr(t), _ptr(mark), _ptr(buf), ctypes.c_size_t(buf.numel()),
+                             _ptr(status), _stream(stream))
+    _check(rc, "mdhp_seq_pack")
+    return PackedSeq(desc, buf, status)
+
+
+def seq_loglik_grad(ps: PackedSeq, theta, alpha, beta, grads=True, stream=None):
+    D = ps.D
+    for nm, x in (("theta", theta), ("alpha", alpha), ("beta", beta)):
+        _dev(x, torch.float32, nm)
+    dev = theta.device
+    lnl = torch.empty(1, dtype=torch.float64, device=dev)
+    gt = torch.empty(D, dtype=torch.float32, device=dev) if grads else None
+    ga = torch.empty(D, D, dtype=torch.float32, device=dev) if grads else None
+    gb = torch.empty(D, D, dtype=torch.float32, device=dev) if grads else None
+    rc = lib().mdhp_seq_loglik_grad(ctypes.byref(ps.desc), _ptr(ps.buf), _ptr(theta), _ptr(alpha), _ptr(beta),
+                                    _ptr(lnl), _ptr(gt), _ptr(ga), _ptr(gb), _stream(stream))
+    _check(rc, "mdhp_seq_loglik_grad")
+    return {"lnl": lnl, "g_theta": gt, "g_alpha": ga, "g_beta": gb}
+
+
+def seq_fit(ps: PackedSeq, theta, alpha, beta, cfg: FitConfig, opt_state=None, trace=False, stream=None):
+    """mdhp_seq_fit; theta [D], alpha/beta [D,D] fp32 CUDA tensors updated in place."""
+    for nm, x in (("theta", theta), ("alpha", alpha), ("beta", beta)):
+        _dev(x, torch.float32, nm)
+    dev = theta.device
+    lnl = torch.empty(1, dtype=torch.float64, device=dev)
+    iters = torch.empty(1, dtype=torch.int32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    tr = torch.empty(max(cfg.max_iters, 1), dtype=torch.float32, device=dev) if trace else None
+    c = cfg.c()
+    rc = lib().mdhp_seq_fit(ctypes.byref(ps.desc), _ptr(ps.buf), ctypes.byref(c), _ptr(theta), _ptr(alpha),
+                            _ptr(beta), _ptr(opt_state), _ptr(lnl), _ptr(iters), _ptr(status), _ptr(tr),
+                            _stream(stream))
+    _check(rc, "mdhp_seq_fit")
+    return {"lnl": lnl, "iters": iters, "status": status, "trace": tr}
