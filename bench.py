@@ -51,8 +51,61 @@ WORKLOADS = {
     # name: (recipe key, windows per GPU)
     "cfg2": ("cfg2", 4096),
     "cfg3": ("cfg3", 65536),
+    "cfg4": ("cfg4", 1),
     "cfg5": ("cfg5", 1 << 20),
 }
+
+
+def bench_seq(args, rc, world, rank, dev):
+    """--config cfg4: one long sequence per GPU (replicas at N > 1: the sequence path does not
+    shard), fitted by the chunked-scan path (mdhp_seq_fit)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2411_10258_b200 as M
+    from synth import gpu as sgpu
+    D = rc.D
+    b = sgpu.make_batch_gpu(rc, 1, seed=args.seed, first_window=rank, device=dev)
+    N = int(b["win_off"][-1])
+    ps = M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=256)
+    th0 = b["theta"][0].clone(); al0 = b["alpha"][0].clone(); be0 = b["beta"][0].clone()
+    th, al, be = th0.clone(), al0.clone(), be0.clone()
+    cfg = M.FitConfig(max_iters=args.iters, optimizer="adam", lr=0.05, tol_rel=0.0)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        th.copy_(th0); al.copy_(al0); be.copy_(be0)
+        M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=256, out=ps)
+        return M.seq_fit(ps, th, al, be, cfg)
+    for _ in range(args.warmup):
+        r = step()
+    torch.cuda.synchronize()
+    evals = int(r["iters"][0]) + 1
+    if world > 1:
+        dist.barrier()
+    L0 = M.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        r = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    value = world * N * evals * args.steps / (float(t_max) / 1e3)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": float(t_max) / args.steps,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                          "data": f"synthetic (Ogata-thinned MDHP on GPU, recipe cfg4, seed {args.seed})",
+                          "config": {"workload": f"cfg4: one sequence/GPU, D={D}, {N} events over {rc.T}s, "
+                                                 f"chunked scan (256 events/chunk), Adam lr 0.05, {args.iters} "
+                                                 "fixed iterations + final eval", "events": N},
+                          "gpu_launches": int(M.launch_count() - L0)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
 
 
 class ClockSampler:
@@ -200,15 +253,18 @@ def main():
     stream = torch.cuda.current_stream()
 
     # ---- synthetic inputs (untimed): windows rank*W .. rank*W+W-1 of the global seeded stream
-    b = sgpu.make_batch_gpu(rc, W, seed=args.seed, first_window=rank * W, device=dev)
+    if args.config == "cfg4":
+        return bench_seq(args, rc, world, rank, dev)
+    first, _ = (rank * W, W)
+    b = sgpu.make_batch_gpu(rc, W, seed=args.seed, first_window=first, device=dev)
     E = int(b["win_off"][-1])
     init_th = torch.full((W, D), 0.1, device=dev)
     init_al = torch.full((W, D, D), 0.5, device=dev)
     init_be = torch.full((W, D, D), 1.0, device=dev)
     th, al, be = init_th.clone(), init_al.clone(), init_be.clone()
     cfg = M.FitConfig(max_iters=args.iters, optimizer="adam", lr=0.05, tol_rel=0.0)
-    rec_cols = D + 2 * D * D + 3
-    rec = torch.empty(W, rec_cols, dtype=torch.float32, device=dev)
+    from paper_2411_10258_b200 import shard
+    rec = torch.empty(W, shard.record_width(D), dtype=torch.float32, device=dev)
     gathered = [torch.empty_like(rec) for _ in range(world)] if (world > 1 and rank == 0) else None
     packed = None
     fit_ev0, fit_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -222,14 +278,9 @@ def main():
         r = M.fit(packed, th, al, be, cfg)
         if timing_fit is not None:
             timing_fit[1].record(stream)
-        if world > 1:
-            rec[:, :D] = th
-            rec[:, D:D + D * D] = al.view(W, -1)
-            rec[:, D + D * D:D + 2 * D * D] = be.view(W, -1)
-            rec[:, -3] = r["lnl"].float()
-            rec[:, -2] = r["iters"].float()
-            rec[:, -1] = r["status"][:W].float()
-            dist.gather(rec, gathered, dst=0)
+        if world > 1:   # a8: one gather of fixed-size per-window records to rank 0
+            shard.pack_records(th, al, be, r["lnl"], r["iters"], r["status"], out=rec)
+            shard.gather_records(rec, world, rank, out=gathered)
         return r
 
     for _ in range(args.warmup):

@@ -79,6 +79,10 @@ extern "C" {
 #define MDHP_TIME_EQ6   2   /* Eq.(6) P:372-374 with the window's joint min/max over all     */
                             /* dims mapped to [eq6_lo, eq6_hi]; horizon eq6_hi */
 
+#define MDHP_TIE_ERROR  0   /* a same-mark tie after fp32 conversion flags SAME_DIM_TIE        */
+#define MDHP_TIE_NUDGE  1   /* in stream order y_k = max(fl32(x_k), y_{k-1}); if the */
+                            /* previous event of the same mark has time y_k, y_k = next float up  */
+
 typedef struct {
     int32_t D;            /* number of marks, 1..32                                         */
     int32_t time_mode;    /* MDHP_TIME_*                                                    */
@@ -86,6 +90,8 @@ typedef struct {
     int64_t n_events;     /* E >= 0 (total over all windows, = win_off[W])                  */
     double  eq6_lo;       /* EQ6 target range (ignored otherwise)                           */
     double  eq6_hi;
+    int32_t tie_policy;   /* MDHP_TIE_ERROR | MDHP_TIE_NUDGE                                */
+    int32_t reserved;     /* 0                                                              */
 } mdhp_pack_desc;
 
 /* Bytes the packed buffer needs for this descriptor (a pure function of D, W, E).          */

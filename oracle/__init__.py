@@ -90,7 +90,7 @@ def lib():
         P = ctypes.c_void_p
         L.oracle_convert_window.restype = ctypes.c_int
         L.oracle_convert_window.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double,
-                                            ctypes.c_double, ctypes.c_int64, P, P,
+                                            ctypes.c_double, ctypes.c_int, ctypes.c_int64, P, P,
                                             ctypes.c_double, P, P]
         for name in ("oracle_loglik_def", "oracle_loglik_rec"):
             f = getattr(L, name)
@@ -117,13 +117,16 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
-def convert_window(D, t, mark, T, time_mode=TIME_RAW, lo=0.0, hi=1.0):
+TIE_ERROR, TIE_NUDGE = 0, 1
+
+
+def convert_window(D, t, mark, T, time_mode=TIME_RAW, lo=0.0, hi=1.0, tie_policy=TIE_ERROR):
     """-> (t32 float32[n], T32 float, status int).  Packing definition (oracle.c)."""
     t = _f64(t)
     mark = np.ascontiguousarray(mark, dtype=np.int32)
     out = np.zeros(len(t), dtype=np.float32)
     T32 = np.zeros(1, dtype=np.float32)
-    st = lib().oracle_convert_window(int(D), int(time_mode), float(lo), float(hi), len(t),
+    st = lib().oracle_convert_window(int(D), int(time_mode), float(lo), float(hi), int(tie_policy), len(t),
                                      _p(t), _p(mark), float(T), _p(out), _p(T32))
     return out, float(T32[0]), int(st)
 

@@ -63,10 +63,11 @@
  * Validation, on the input order:  T finite and > 0 (else BAD_T); every t finite with
  * 0 <= t <= T (else OUT_OF_RANGE); 0 <= mark < D (else BAD_MARK); t non-decreasing
  * (else UNSORTED); after rounding, no two events of the same mark share a t32
- * (else SAME_DIM_TIE, S:106 / DESIGN.md R10); EQ6 with mx == mn -> DEGENERATE.
+ * (else SAME_DIM_TIE, S:106 / DESIGN.md R10; with tie_policy NUDGE such events are moved up
+ * instead, see below); EQ6 with mx == mn -> DEGENERATE.
  * An empty window is valid (status EMPTY).  Returns the status word.
  * ------------------------------------------------------------------------------------- */
-int oracle_convert_window(int D, int time_mode, double lo, double hi, int64_t n,
+int oracle_convert_window(int D, int time_mode, double lo, double hi, int tie_policy, int64_t n,
                           const double* t, const int32_t* mark, double T,
                           float* t32_out, float* T32_out)
 {
@@ -94,6 +95,23 @@ int oracle_convert_window(int D, int time_mode, double lo, double hi, int64_t n,
         t32_out[k] = (float)x;
     }
     *T32_out = (float)Tp;
+    /* tie_policy 1 = NUDGE, the rule of include/mdhp.h MDHP_TIE_NUDGE, applied
+       literally in stream order: y_k = max(fl32(x_k), y_{k-1}); if the previous event of the same
+       mark has time y_k, y_k = nextafterf(y_k, +inf). */
+    if (tie_policy == 1 && !(status & (OR_BAD_MARK | OR_UNSORTED))) {
+        float floor_ = -INFINITY;
+        for (int64_t k = 0; k < n; k++) {
+            float y = t32_out[k] > floor_ ? t32_out[k] : floor_;
+            for (int64_t q = k - 1; q >= 0; q--) {        /* previous event of the same mark */
+                if (mark[q] == mark[k]) {
+                    if (t32_out[q] == y) y = nextafterf(y, INFINITY);
+                    break;
+                }
+            }
+            t32_out[k] = y;
+            floor_ = y;
+        }
+    }
     /* same-dim ties after rounding: compare every pair of events with equal mark that
        are adjacent among that mark's events (plain O(N*D) scan, no cleverness). */
     if (!(status & (OR_BAD_MARK | OR_UNSORTED))) {

@@ -57,6 +57,10 @@ static int check_desc(const mdhp_pack_desc* d) {
     set_error("bad time_mode %d", d->time_mode);
     return MDHP_EINVAL;
   }
+  if (d->tie_policy != MDHP_TIE_ERROR && d->tie_policy != MDHP_TIE_NUDGE) {
+    set_error("bad tie_policy %d", d->tie_policy);
+    return MDHP_EINVAL;
+  }
   if (d->time_mode == MDHP_TIME_EQ6 && !(d->eq6_hi > d->eq6_lo)) {
     set_error("EQ6 needs eq6_hi > eq6_lo (S:128)");
     return MDHP_EINVAL;

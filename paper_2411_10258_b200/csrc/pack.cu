@@ -17,7 +17,7 @@ __device__ __forceinline__ int64_t round8(int64_t x) { return (x + 7) & ~int64_t
 
 // One warp per window.  Pass 1 (EQ6 only): joint min/max.  Pass 2: chunks of 32 events.
 __global__ void __launch_bounds__(kPackWPB * 32)
-k_pack_events(int D, int Dp, int mode, double lo, double hi, int64_t W,
+k_pack_events(int D, int Dp, int mode, double lo, double hi, int nudge, int64_t W,
               const double* __restrict__ t, const int32_t* __restrict__ mark,
               const int64_t* __restrict__ off, const double* __restrict__ Tin,
               int64_t* __restrict__ o_begin, int32_t* __restrict__ o_n, float* __restrict__ o_T32,
@@ -105,6 +105,35 @@ k_pack_events(int D, int Dp, int mode, double lo, double hi, int64_t W,
   }
   st = __reduce_or_sync(kFull, st);
   if (st & (MDHP_ST_UNSORTED | MDHP_ST_BAD_MARK)) st &= ~MDHP_ST_SAME_DIM_TIE;
+  if (nudge && (st & MDHP_ST_SAME_DIM_TIE)) {
+    // MDHP_TIE_NUDGE: sequential fix-up of this window only (rare), in stream
+    // order: y_k = max(fl32(x_k), y_{k-1}); a tie with the previous event of the same mark moves
+    // y_k to the next float up.  Rewrites times, gaps and first times.
+    st &= ~MDHP_ST_SAME_DIM_TIE;
+    if (lane == 0) {
+      float lastm[32];
+      bool have[32];
+      for (int q = 0; q < 32; q++) have[q] = false;
+      float floor_ = -INFINITY;
+      for (int64_t k = 0; k < n; k++) {
+        const double tk = t[a + k];
+        double x = tk;
+        if (mode == MDHP_TIME_UNIT) x = __ddiv_rn(tk, T);
+        else if (mode == MDHP_TIME_EQ6)
+          x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(tk, mn), __dsub_rn(mx, mn)), __dsub_rn(hi, lo)), lo);
+        float y = fmaxf(__double2float_rn(x), floor_);
+        const int mk = mark[a + k];
+        if (have[mk] && lastm[mk] == y) y = nextafterf(y, INFINITY);
+        o_t32[beg + k] = y;
+        o_dtp[beg + k] = __fsub_rn(y, have[mk] ? lastm[mk] : -1.0f);
+        if (!have[mk]) s_first[wp][mk] = y;
+        lastm[mk] = y;
+        have[mk] = true;
+        floor_ = y;
+      }
+    }
+    __syncwarp();
+  }
   const int64_t npad = round8(n);
   for (int64_t k = n + lane; k < npad; k += 32) {   // null events (eval.cuh: kNullT)
     o_t32[beg + k] = -2.0f;
@@ -238,7 +267,7 @@ int pack_launch(const mdhp_pack_desc* d, const double* t, const int32_t* mark,
 
   const unsigned blocks = (unsigned)((W + kPackWPB - 1) / kPackWPB);
   k_pack_events<<<blocks, kPackWPB * 32, 0, st>>>(d->D, L.Dp, d->time_mode, d->eq6_lo, d->eq6_hi,
-                                                  W, t, mark, win_off, T, o_begin, o_n, o_T32,
+                                                  d->tie_policy == MDHP_TIE_NUDGE, W, t, mark, win_off, T, o_begin, o_n, o_T32,
                                                   o_t32, o_dtp, o_mark, o_cnt, o_umax, win_status);
   k_pack_moments<<<blocks, kPackWPB * 32, 0, st>>>(d->D, L.Dp, W, o_begin, o_n, o_T32, o_t32,
                                                    o_mark, o_umax, o_mom, win_status);

@@ -19,6 +19,7 @@ ST_OK, ST_EMPTY, ST_UNSORTED, ST_OUT_OF_RANGE, ST_BAD_MARK = 0, 1, 2, 4, 8
 ST_SAME_DIM_TIE, ST_DEGENERATE, ST_NONFINITE, ST_DIVERGED, ST_CONVERGED, ST_BAD_T = 16, 32, 64, 128, 256, 512
 ST_INVALID = ST_UNSORTED | ST_OUT_OF_RANGE | ST_BAD_MARK | ST_SAME_DIM_TIE | ST_DEGENERATE | ST_BAD_T
 TIME_RAW, TIME_UNIT, TIME_EQ6 = 0, 1, 2
+TIE_ERROR, TIE_NUDGE = 0, 1
 OPT_GD, OPT_ADAM = 0, 1
 FIT_THETA, FIT_ALPHA, FIT_BETA = 1, 2, 4
 
@@ -26,7 +27,8 @@ FIT_THETA, FIT_ALPHA, FIT_BETA = 1, 2, 4
 class PackDesc(ctypes.Structure):
     _fields_ = [("D", ctypes.c_int32), ("time_mode", ctypes.c_int32),
                 ("n_windows", ctypes.c_int64), ("n_events", ctypes.c_int64),
-                ("eq6_lo", ctypes.c_double), ("eq6_hi", ctypes.c_double)]
+                ("eq6_lo", ctypes.c_double), ("eq6_hi", ctypes.c_double),
+                ("tie_policy", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class SeqDesc(ctypes.Structure):
@@ -153,8 +155,8 @@ class Packed:
         return int(self.desc.n_windows)
 
 
-def make_desc(D, W, E, time_mode=TIME_RAW, eq6_lo=0.0, eq6_hi=1.0) -> PackDesc:
-    return PackDesc(int(D), int(time_mode), int(W), int(E), float(eq6_lo), float(eq6_hi))
+def make_desc(D, W, E, time_mode=TIME_RAW, eq6_lo=0.0, eq6_hi=1.0, tie_policy=TIE_NUDGE) -> PackDesc:
+    return PackDesc(int(D), int(time_mode), int(W), int(E), float(eq6_lo), float(eq6_hi), int(tie_policy), 0)
 
 
 def packed_layout(desc: PackDesc) -> dict:
@@ -189,12 +191,12 @@ def packed_bytes(desc: PackDesc) -> int:
 
 
 def pack_windows(D, t, mark, win_off, T, time_mode=TIME_RAW, eq6_lo=0.0, eq6_hi=1.0,
-                 out: Packed | None = None, stream=None) -> Packed:
+                 out: Packed | None = None, tie_policy=TIE_NUDGE, stream=None) -> Packed:
     """mdhp_pack_windows on CUDA tensors t f64[E], mark i32[E], win_off i64[W+1], T f64[W]."""
     _dev(t, torch.float64, "t"); _dev(mark, torch.int32, "mark")
     _dev(win_off, torch.int64, "win_off"); _dev(T, torch.float64, "T")
     W = T.numel(); E = t.numel()
-    desc = make_desc(D, W, E, time_mode, eq6_lo, eq6_hi)
+    desc = make_desc(D, W, E, time_mode, eq6_lo, eq6_hi, tie_policy)
     nb = packed_bytes(desc)
     if nb == 0:
         _check(-2, "mdhp_packed_bytes")
@@ -250,7 +252,7 @@ def fit(pk: Packed, theta, alpha, beta, cfg: FitConfig, opt_state=None, trace=Fa
 
 
 def fit_host(D, t, mark, win_off, T, theta, alpha, beta, cfg: FitConfig, time_mode=TIME_RAW,
-             eq6_lo=0.0, eq6_hi=1.0, stream=None):
+             eq6_lo=0.0, eq6_hi=1.0, tie_policy=TIE_NUDGE, stream=None):
     """mdhp_fit_host on CPU tensors (pinned recommended).  theta/alpha/beta updated in place;
     returns dict with lnl, iters, status (CPU tensors)."""
     for nm, x, dt in (("t", t, torch.float64), ("mark", mark, torch.int32), ("win_off", win_off, torch.int64),
@@ -259,7 +261,7 @@ def fit_host(D, t, mark, win_off, T, theta, alpha, beta, cfg: FitConfig, time_mo
         if x.is_cuda or x.dtype != dt or not x.is_contiguous():
             raise TypeError(f"{nm} must be a contiguous CPU {dt} tensor")
     W = T.numel()
-    desc = make_desc(D, W, t.numel(), time_mode, eq6_lo, eq6_hi)
+    desc = make_desc(D, W, t.numel(), time_mode, eq6_lo, eq6_hi, tie_policy)
     lnl = torch.empty(W, dtype=torch.float64)
     iters = torch.empty(W, dtype=torch.int32)
     status = torch.empty(W, dtype=torch.int32)

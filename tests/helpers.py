@@ -41,7 +41,7 @@ def random_params(rng, W, D, scale_theta=(0.5, 30.0), alpha=(0.0, 8.0), beta=(0.
     return th, al, be
 
 
-def oracle_times(b, D, time_mode=oracle.TIME_RAW, lo=0.0, hi=1.0):
+def oracle_times(b, D, time_mode=oracle.TIME_RAW, lo=0.0, hi=1.0, tie_policy=oracle.TIE_NUDGE):
     """Oracle's own packing of every window -> (t32 concat, T32 per window, status per window)."""
     W = len(b["win_off"]) - 1
     t32 = np.zeros(len(b["t"]), np.float32)
@@ -49,7 +49,8 @@ def oracle_times(b, D, time_mode=oracle.TIME_RAW, lo=0.0, hi=1.0):
     st = np.zeros(W, np.int32)
     for w in range(W):
         a, z = b["win_off"][w], b["win_off"][w + 1]
-        o, T_, s = oracle.convert_window(D, b["t"][a:z], b["mark"][a:z], b["T"][w], time_mode, lo, hi)
+        o, T_, s = oracle.convert_window(D, b["t"][a:z], b["mark"][a:z], b["T"][w], time_mode, lo, hi,
+                                         tie_policy)
         t32[a:z] = o
         T32[w] = T_
         st[w] = s

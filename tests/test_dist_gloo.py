@@ -1,0 +1,83 @@
+"""Multi-process (world size 2, gloo, CPU) coverage of the sharding/gather host logic (row a8).
+The data path itself has no collective; this checks what crosses processes."""
+import os
+import socket
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2411_10258_b200 import shard
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _fake_results(rank, W, D):
+    g = torch.Generator().manual_seed(100 + rank)
+    th = torch.rand(W, D, generator=g)
+    al = torch.rand(W, D, D, generator=g)
+    be = torch.rand(W, D, D, generator=g)
+    lnl = torch.randn(W, generator=g, dtype=torch.float64) * 1e4
+    it = torch.arange(W, dtype=torch.int32) + 7 * rank
+    st = torch.full((W,), 256 * rank + 1, dtype=torch.int32)
+    return th, al, be, lnl, it, st
+
+
+def _worker(rank, world, port, W, D, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    first, n = shard.weak_range(W, rank)
+    rec = shard.pack_records(*_fake_results(rank, W, D))
+    got = shard.gather_records(rec, world, rank)
+    if rank == 0:
+        ok = True
+        for r in range(world):
+            u = shard.unpack_records(got[r], D)
+            ref = _fake_results(r, W, D)
+            ok &= torch.equal(u["theta"], ref[0]) and torch.equal(u["alpha"], ref[1])
+            ok &= torch.equal(u["beta"], ref[2]) and torch.equal(u["lnl"], ref[3])
+            ok &= torch.equal(u["iters"], ref[4]) and torch.equal(u["status"], ref[5])
+        q.put(("ok" if ok else "mismatch", first, n))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    W, D = 37, 5
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, W, D, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+        assert p.exitcode == 0
+    status, first, n = q.get(timeout=5)
+    assert status == "ok" and first == 0 and n == W
+
+
+def test_records_roundtrip_bit_exact():
+    th, al, be, lnl, it, st = _fake_results(3, 11, 4)
+    u = shard.unpack_records(shard.pack_records(th, al, be, lnl, it, st), 4)
+    assert torch.equal(u["lnl"], lnl) and torch.equal(u["status"], st) and torch.equal(u["beta"], be)
+
+
+def test_balanced_ranges():
+    rng = np.random.default_rng(0)
+    c = rng.poisson(1000, 10000)
+    for world in (1, 2, 4, 8):
+        rr = shard.balanced_ranges(c, world)
+        assert rr[0][0] == 0 and rr[-1][1] == len(c)
+        assert all(rr[k][1] == rr[k + 1][0] for k in range(world - 1))
+        loads = [c[a:b].sum() for a, b in rr]
+        assert max(loads) - min(loads) <= 2 * c.max()
+    assert shard.balanced_ranges([5, 0, 0], 4)[-1] == (3, 3) or shard.balanced_ranges([5, 0, 0], 4)[-1][1] == 3

@@ -28,8 +28,8 @@ def f32(x):
     return np.asarray(x, np.float32)
 
 
-def gpu_loglik(D, b, th, al, be, time_mode=mdhp.TIME_RAW, grads=True):
-    pk = M.pack_windows(D, *dev_batch(b), time_mode=time_mode)
+def gpu_loglik(D, b, th, al, be, time_mode=mdhp.TIME_RAW, grads=True, tie_policy=mdhp.TIE_NUDGE):
+    pk = M.pack_windows(D, *dev_batch(b), time_mode=time_mode, tie_policy=tie_policy)
     r = M.loglik_grad(pk, torch.tensor(f32(th), device=DEV), torch.tensor(f32(al), device=DEV),
                       torch.tensor(f32(be), device=DEV), grads=grads)
     torch.cuda.synchronize()
@@ -55,14 +55,13 @@ def test_pack_parity(D):
     wins = [(b["t"][b["win_off"][w]:b["win_off"][w + 1]], b["mark"][b["win_off"][w]:b["win_off"][w + 1]])
             for w in range(len(b["T"]))] + invalid_windows(D)
     b = H.batch_from_windows(wins, 1.0)
-    for mode in (mdhp.TIME_RAW, mdhp.TIME_UNIT, mdhp.TIME_EQ6):
+    for mode, tie in ((mdhp.TIME_RAW, 0), (mdhp.TIME_RAW, 1), (mdhp.TIME_UNIT, 1), (mdhp.TIME_EQ6, 0),
+                      (mdhp.TIME_EQ6, 1)):
         bb = dict(b)
-        if mode == mdhp.TIME_UNIT:
-            bb["T"] = b["T"] * 1.0
-        pk = M.pack_windows(D, *dev_batch(bb), time_mode=mode, eq6_lo=0.0, eq6_hi=1.0)
+        pk = M.pack_windows(D, *dev_batch(bb), time_mode=mode, eq6_lo=0.0, eq6_hi=1.0, tie_policy=tie)
         v = {k: (x.cpu().numpy() if torch.is_tensor(x) else x) for k, x in mdhp.unpack_views(pk).items()}
         st = pk.status.cpu().numpy()
-        t32, T32, st_o = H.oracle_times(bb, D, mode, 0.0, 1.0)
+        t32, T32, st_o = H.oracle_times(bb, D, mode, 0.0, 1.0, tie)
         W = len(bb["T"])
         np.testing.assert_array_equal(st[:W], st_o)
         for w in range(W):
@@ -148,8 +147,10 @@ def test_invalid_and_empty_windows():
     b = H.batch_from_windows(wins, 1.0)
     W = len(wins)
     th = np.full((W, D), 0.7); al = np.full((W, D, D), 0.3); be = np.full((W, D, D), 2.0)
-    out, _ = gpu_loglik(D, b, th, al, be)
+    out, _ = gpu_loglik(D, b, th, al, be, tie_policy=mdhp.TIE_ERROR)
     assert np.all(np.isnan(out["lnl"][:4])) and np.all(np.isnan(out["g_alpha"][:4]))
+    out2, _ = gpu_loglik(D, b, th, al, be, tie_policy=mdhp.TIE_NUDGE)   # the tie window is nudged
+    assert np.all(np.isnan(out2["lnl"][:3])) and np.isfinite(out2["lnl"][3])
     assert out["status"][4] == mdhp.ST_EMPTY
     assert out["lnl"][4] == pytest.approx(-float(f32(0.7)) * 3, rel=1e-7)
     np.testing.assert_allclose(out["g_theta"][4], -1.0)

@@ -125,6 +125,17 @@ def test_convert_validation_statuses():
     assert cw(1, [0.5, 0.5 + 1e-12], [0, 0], 1.0)[2] & oracle.SAME_DIM_TIE
     assert cw(2, [0.3, 0.3], [0, 1], 1.0, oracle.TIME_EQ6)[2] & oracle.DEGENERATE
     assert cw(2, [0.1], [0], 0.0)[2] & oracle.BAD_T
+    # NUDGE: y_k = max(fl32(x_k), y_{k-1}); a tie with the previous event of the
+    # same mark moves to the next float.  Hand example: marks 0,0,1,1 all at x = 0.5:
+    # 0.5, 0.5+u, then mark 1 starts at max(0.5, 0.5+u) = 0.5+u, its second event ties -> 0.5+2u.
+    x = np.float32(0.5)
+    u1 = np.nextafter(x, np.float32(2)); u2 = np.nextafter(u1, np.float32(2))
+    out, _, st = cw(2, [0.5, 0.5, 0.5, 0.5], [0, 0, 1, 1], 1.0, tie_policy=oracle.TIE_NUDGE)
+    assert st == oracle.OK
+    np.testing.assert_array_equal(out, np.array([x, u1, u1, u2], np.float32))
+    out, _, st = cw(2, [0.25, 0.5, 0.5 + 1e-12, 0.75], [1, 0, 0, 1], 1.0, tie_policy=oracle.TIE_NUDGE)
+    np.testing.assert_array_equal(out, np.array([0.25, x, u1, 0.75], np.float32))
+    assert cw(2, [0.5, 0.5], [0, 0], 1.0, tie_policy=oracle.TIE_NUDGE)[2] == oracle.OK
     out, T32, st = cw(1, [0.1, 0.3], [0, 0], 3.0, oracle.TIME_UNIT)
     np.testing.assert_array_equal(out, np.array([0.1 / 3.0, 0.3 / 3.0], np.float32))
     assert T32 == 1.0
