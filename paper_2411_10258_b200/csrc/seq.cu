@@ -20,7 +20,7 @@
 namespace mdhp {
 
 constexpr int kSeqWPB = 4;
-constexpr int kScanSeg = 64;
+constexpr int kScanSeg = 256;
 
 struct SeqLayout {
   int D, Dp;
@@ -153,29 +153,40 @@ k_seq_events(int D, int Dp, int64_t N, int64_t C, double T, const double* __rest
   }
 }
 
-// One warp: per-mark totals, first times -> u_max, and the tail T - (last event).
-__global__ void k_seq_stats(int D, int Dp, int64_t N, int64_t C, double T,
-                            const double* __restrict__ t, const int32_t* __restrict__ ccnt,
-                            const double* __restrict__ cfirst, int32_t* __restrict__ cnt,
-                            float* __restrict__ umax, float* __restrict__ tail,
-                            int32_t* __restrict__ status) {
-  const int j = threadIdx.x;
-  if (j < Dp) {
-    int tot = 0;
-    double first = 0.0;
-    bool have = false;
-    for (int64_t c = 0; c < C; c++) {
-      const int k = ccnt[c * Dp + j];
-      if (k > 0 && !have) {
-        first = cfirst[c * Dp + j];
-        have = true;
-      }
-      tot += k;
-    }
-    cnt[j] = j < D ? tot : 0;
-    umax[j] = (j < D && tot > 0) ? __double2float_rn(__dsub_rn(T, first)) : 0.0f;
+// Per-mark totals, first times -> u_max, and the tail T - (last event).  One block of 256
+// threads over chunks; integer sums and a min over chunk indices are order-independent.
+__global__ void __launch_bounds__(256)
+k_seq_stats(int D, int Dp, int64_t N, int64_t C, double T, const double* __restrict__ t,
+            const int32_t* __restrict__ ccnt, const double* __restrict__ cfirst,
+            int32_t* __restrict__ cnt, float* __restrict__ umax, float* __restrict__ tail,
+            int32_t* __restrict__ status) {
+  __shared__ int s_cnt[32];
+  __shared__ unsigned long long s_firstc[32];
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    s_cnt[tid] = 0;
+    s_firstc[tid] = ~0ull;
   }
-  if (j == 0) {
+  __syncthreads();
+  for (int j = 0; j < Dp; j++) {
+    int tot = 0;
+    unsigned long long fc = ~0ull;
+    for (int64_t c = tid; c < C; c += blockDim.x) {
+      const int k = ccnt[c * Dp + j];
+      tot += k;
+      if (k > 0 && (unsigned long long)c < fc) fc = (unsigned long long)c;
+    }
+    if (tot) atomicAdd(&s_cnt[j], tot);
+    if (fc != ~0ull) atomicMin(&s_firstc[j], fc);
+  }
+  __syncthreads();
+  if (tid < Dp) {
+    const int j = tid;
+    const int tot = j < D ? s_cnt[j] : 0;
+    cnt[j] = tot;
+    umax[j] = (tot > 0) ? __double2float_rn(__dsub_rn(T, cfirst[(int64_t)s_firstc[j] * Dp + j])) : 0.0f;
+  }
+  if (tid == 0) {
     tail[0] = N > 0 ? __double2float_rn(__dsub_rn(T, t[N - 1])) : (float)T;
     tail[1] = (float)T;
     if (!(T > 0.0) || !isfinite(T)) atomicOr(status, MDHP_ST_BAD_T);
@@ -221,13 +232,19 @@ k_seq_moments(int D, int Dp, int64_t C, double T, const double* __restrict__ t,
   }
 }
 
-__global__ void k_seq_momsum(int Dp, int64_t C, const float* __restrict__ cmom,
-                             float* __restrict__ mom) {
-  const int q = threadIdx.x;   // (mark, p)
-  if (q >= Dp * kMom) return;
+__global__ void __launch_bounds__(256)
+k_seq_momsum(int Dp, int64_t C, const float* __restrict__ cmom, float* __restrict__ mom) {
+  __shared__ double red[256];
+  const int q = blockIdx.x;   // (mark, p)
   double s = 0.0;
-  for (int64_t c = 0; c < C; c++) s += (double)cmom[c * Dp * kMom + q];
-  mom[q] = (float)s;
+  for (int64_t c = threadIdx.x; c < C; c += 256) s += (double)cmom[c * Dp * kMom + q];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o >= 1; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) mom[q] = (float)red[0];
 }
 
 // ---------------------------------------------------------------- evaluation workspace
@@ -244,6 +261,7 @@ struct SeqWork {
   int* ctl;        // optimizer control block (seq fit)
   float* prev;     // [D + 2 D^2] previous point (rollback)
   float* opt;      // [2 (D + 2 D^2)] Adam moments when the caller passes none
+  double* rpart;   // [kRedBlocks][2 D^2 + D + 1] stage-1 partial sums
   size_t bytes;
 };
 
@@ -256,7 +274,8 @@ inline SeqWork make_seq_work(void* base, int D, int Dp, int64_t C) {
                f = take(sizeof(float2) * DD), g = take(sizeof(float2) * C * DD),
                h = take(sizeof(float) * C * Dp), l = take(sizeof(double) * (C + 1)),
                gs = take(sizeof(float2) * DD), gt = take(sizeof(float) * Dp), ls = take(sizeof(double)),
-               ct = take(sizeof(int) * 64), pv = take(sizeof(float) * P), op = take(sizeof(float) * 2 * P);
+               ct = take(sizeof(int) * 64), pv = take(sizeof(float) * P), op = take(sizeof(float) * 2 * P),
+               rp = take(sizeof(double) * 128 * (2 * DD + D + 1));
   char* B = static_cast<char*>(base);
   w.loc = reinterpret_cast<float2*>(B + a);
   w.carry = reinterpret_cast<float2*>(B + b);
@@ -270,6 +289,7 @@ inline SeqWork make_seq_work(void* base, int D, int Dp, int64_t C) {
   w.ctl = reinterpret_cast<int*>(B + ct);
   w.prev = reinterpret_cast<float*>(B + pv);
   w.opt = reinterpret_cast<float*>(B + op);
+  w.rpart = reinterpret_cast<double*>(B + rp);
   w.bytes = o;
   return w;
 }
@@ -340,46 +360,58 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
 }
 
 // Phase 2: exclusive scan of the per-chunk affine maps, one block per pair, kScanSeg segments.
+// A map over a stretch of span L is x -> (E S + Sb, E (Q + L S) + Qb), E = e^{-beta L};
+// composing "m1 then m2" gives E = E2 E1, L = L1 + L2, Sb = E2 Sb1 + Sb2,
+// Qb = E2 (Qb1 + L2 Sb1) + Qb2 (associative), so segments are scanned in log2(kScanSeg) rounds.
+struct AffMap {
+  float E, L, Sb, Qb;
+};
+__device__ __forceinline__ AffMap compose(const AffMap& m1, const AffMap& m2) {
+  AffMap r;
+  r.E = m2.E * m1.E;
+  r.L = m1.L + m2.L;
+  r.Sb = fmaf(m2.E, m1.Sb, m2.Sb);
+  r.Qb = fmaf(m2.E, fmaf(m2.L, m1.Sb, m1.Qb), m2.Qb);
+  return r;
+}
+
 __global__ void __launch_bounds__(kScanSeg)
 k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __restrict__ beta,
            const float2* __restrict__ loc, float2* __restrict__ carry, float2* __restrict__ fin,
            const int* __restrict__ ctl) {
   if (ctl && ctl[0]) return;
-  __shared__ float2 sx[kScanSeg];
-  __shared__ float sl[kScanSeg];
-  __shared__ float2 sc[kScanSeg + 1];
+  __shared__ AffMap sm[kScanSeg];
   const int p = blockIdx.x, s = threadIdx.x;
   const size_t DD = (size_t)D * D;
   const float b = beta[p];
   const int64_t per = (C + kScanSeg - 1) / kScanSeg;
   const int64_t c0 = min(C, (int64_t)s * per), c1 = min(C, c0 + per);
-  auto step = [&](float2 x, float L, float2 l) {
-    const float e = ex2f(b * (L * -kLog2e));
-    return make_float2(fmaf(e, x.x, l.x), fmaf(e, fmaf(L, x.x, x.y), l.y));
-  };
-  float2 x = make_float2(0.0f, 0.0f);
-  float Ls = 0.0f;
+  AffMap m{1.0f, 0.0f, 0.0f, 0.0f};
   for (int64_t c = c0; c < c1; c++) {
-    x = step(x, cspan[c], loc[c * DD + p]);
-    Ls += cspan[c];
+    const float L = cspan[c];
+    const float2 l = loc[c * DD + p];
+    const AffMap mc{ex2f(b * (L * -kLog2e)), L, l.x, l.y};
+    m = compose(m, mc);
   }
-  sx[s] = x;
-  sl[s] = Ls;
+  sm[s] = m;
   __syncthreads();
-  if (s == 0) {
-    float2 y = make_float2(0.0f, 0.0f);
-    for (int q = 0; q < kScanSeg; q++) {
-      sc[q] = y;
-      y = step(y, sl[q], sx[q]);
-    }
-    sc[kScanSeg] = y;
-    fin[p] = y;
+  for (int o = 1; o < kScanSeg; o <<= 1) {   // inclusive Hillis-Steele scan of the maps
+    AffMap prev = m;
+    if (s >= o) prev = compose(sm[s - o], m);
+    __syncthreads();
+    m = prev;
+    sm[s] = m;
+    __syncthreads();
   }
-  __syncthreads();
-  x = sc[s];
+  // state entering segment s = (inclusive map of segment s-1) applied to the zero state
+  float2 x = s > 0 ? make_float2(sm[s - 1].Sb, sm[s - 1].Qb) : make_float2(0.0f, 0.0f);
+  if (s == kScanSeg - 1) fin[p] = make_float2(m.Sb, m.Qb);
   for (int64_t c = c0; c < c1; c++) {
     carry[c * DD + p] = x;
-    x = step(x, cspan[c], loc[c * DD + p]);
+    const float L = cspan[c];
+    const float2 l = loc[c * DD + p];
+    const float e = ex2f(b * (L * -kLog2e));
+    x = make_float2(fmaf(e, x.x, l.x), fmaf(e, fmaf(L, x.x, x.y), l.y));
   }
 }
 
@@ -442,46 +474,51 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
   }
 }
 
-// Phase 4a: fixed-order sums over chunks.  Blocks 0..D^2-1: pair p; block D^2: g_theta, lsum.
+// Phase 4a: fixed-order sums over chunks in two stages (both deterministic).  Elements:
+// 2 D^2 gradient accumulators, D g_theta sums, 1 lsum.  Stage 1: block b sums its contiguous
+// range of chunks for every element (threads over elements: coalesced rows); stage 2: one block
+// sums the kRedBlocks partials per element.
+constexpr int kRedBlocks = 128;
+
 __global__ void __launch_bounds__(256)
-k_seq_reduce(int D, int Dp, int64_t C, const float2* __restrict__ gpart,
-             const float* __restrict__ gthp, const double* __restrict__ lsp,
-             float2* __restrict__ gsum, float* __restrict__ gth, double* __restrict__ ls,
-             int grad, const int* __restrict__ ctl) {
+k_seq_reduce1(int D, int Dp, int64_t C, const float2* __restrict__ gpart,
+              const float* __restrict__ gthp, const double* __restrict__ lsp,
+              double* __restrict__ part, int grad, const int* __restrict__ ctl) {
   if (ctl && ctl[0] == 1 && grad) return;
-  __shared__ double sa[256], sbv[256];
-  const int tid = threadIdx.x;
-  const size_t DD = (size_t)D * D;
-  const int p = blockIdx.x;
-  double a = 0.0, b = 0.0;
-  if (p < (int)DD) {
-    if (!grad) return;
-    for (int64_t c = tid; c < C; c += 256) {
-      const float2 v = gpart[c * DD + p];
-      a += v.x;
-      b += v.y;
+  const int DD = D * D, NE = 2 * DD + D + 1;
+  const int64_t per = (C + kRedBlocks - 1) / kRedBlocks;
+  const int64_t c0 = min(C, (int64_t)blockIdx.x * per), c1 = min(C, c0 + per);
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    double acc = 0.0;
+    if (e < 2 * DD) {
+      if (grad) {
+        const float* gp = reinterpret_cast<const float*>(gpart);
+        for (int64_t c = c0; c < c1; c++) acc += (double)gp[c * 2 * DD + e];
+      }
+    } else if (e < 2 * DD + D) {
+      if (grad)
+        for (int64_t c = c0; c < c1; c++) acc += (double)gthp[c * Dp + (e - 2 * DD)];
+    } else {
+      for (int64_t c = c0; c < c1; c++) acc += lsp[c];
     }
-  } else {
-    for (int64_t c = tid; c < C; c += 256) a += lsp[c];
+    part[(size_t)blockIdx.x * NE + e] = acc;
   }
-  sa[tid] = a;
-  sbv[tid] = b;
-  __syncthreads();
-  for (int o = 128; o >= 1; o >>= 1) {
-    if (tid < o) {
-      sa[tid] += sa[tid + o];
-      sbv[tid] += sbv[tid + o];
-    }
-    __syncthreads();
-  }
-  if (p < (int)DD) {
-    if (tid == 0) gsum[p] = make_float2((float)sa[0], (float)sbv[0]);
-  } else {
-    if (tid == 0) ls[0] = sa[0];
-    if (grad && tid < D) {
-      double s = 0.0;
-      for (int64_t c = 0; c < C; c++) s += gthp[c * Dp + tid];
-      gth[tid] = (float)s;
+}
+
+__global__ void __launch_bounds__(1024)
+k_seq_reduce2(int D, const double* __restrict__ part, float2* __restrict__ gsum,
+              float* __restrict__ gth, double* __restrict__ ls, int grad, const int* __restrict__ ctl) {
+  if (ctl && ctl[0] == 1 && grad) return;
+  const int DD = D * D, NE = 2 * DD + D + 1;
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    double acc = 0.0;
+    for (int q = 0; q < kRedBlocks; q++) acc += part[(size_t)q * NE + e];
+    if (e < 2 * DD) {
+      if (grad) reinterpret_cast<float*>(gsum)[e] = (float)acc;
+    } else if (e < 2 * DD + D) {
+      if (grad) gth[e - 2 * DD] = (float)acc;
+    } else {
+      ls[0] = acc;
     }
   }
 }
@@ -688,7 +725,7 @@ int seq_pack_launch(int D, int64_t N, int ce, double T, const double* t, const i
         at<int32_t>(packed, L.status));
     count_launch(2);
   }
-  k_seq_stats<<<1, 32, 0, st>>>(D, L.Dp, N, C, T, t, at<int32_t>(packed, L.ccnt),
+  k_seq_stats<<<1, 256, 0, st>>>(D, L.Dp, N, C, T, t, at<int32_t>(packed, L.ccnt),
                                 at<double>(packed, L.cfirst), at<int32_t>(packed, L.cnt),
                                 at<float>(packed, L.umax), at<float>(packed, L.tail),
                                 at<int32_t>(packed, L.status));
@@ -702,8 +739,8 @@ int seq_pack_launch(int D, int64_t N, int ce, double T, const double* t, const i
   if (cudaMemsetAsync(at<float>(packed, L.mom), 0, sizeof(float) * L.Dp * kMom, st) != cudaSuccess)
     return MDHP_ECUDA;
   if (C > 0) {
-    k_seq_momsum<<<1, ((L.Dp * kMom + 31) / 32) * 32, 0, st>>>(L.Dp, C, at<float>(packed, L.cmom),
-                                                               at<float>(packed, L.mom));
+    k_seq_momsum<<<L.Dp * kMom, 256, 0, st>>>(L.Dp, C, at<float>(packed, L.cmom),
+                                              at<float>(packed, L.mom));
     count_launch(1);
   }
   if (status_out &&
@@ -755,9 +792,10 @@ static void seq_phases(const SeqLayout& L, const void* pk, const float* th, cons
 static void seq_reduce(const SeqLayout& L, const SeqWork& w, int grad, const int* ctl,
                        cudaStream_t st) {
   if (L.C == 0) return;
-  k_seq_reduce<<<L.D * L.D + 1, 256, 0, st>>>(L.D, L.Dp, L.C, w.gpart, w.gthp, w.lsp, w.gsum,
-                                               w.gth, w.ls, grad, ctl);
-  count_launch(1);
+  k_seq_reduce1<<<kRedBlocks, 256, 0, st>>>(L.D, L.Dp, L.C, w.gpart, w.gthp, w.lsp, w.rpart, grad,
+                                            ctl);
+  k_seq_reduce2<<<1, 1024, 0, st>>>(L.D, w.rpart, w.gsum, w.gth, w.ls, grad, ctl);
+  count_launch(2);
 }
 
 static size_t seq_work_bytes(const SeqLayout& L) {
