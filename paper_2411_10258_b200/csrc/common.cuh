@@ -9,6 +9,8 @@
 namespace mdhp {
 
 constexpr int kAlignEv = 8;     // window event ranges start on 8-event boundaries
+constexpr int kWinStride = 16;  // begin(w) = roundup8(win_off[w]) + 16 w: every window is
+                                // followed by its padding to 8 and 8 null events (eval.cuh)
 constexpr int kMom = 17;        // power moments m_1..m_17 of u/u_max per (window, mark)
 constexpr int kSortBuckets = 65536;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -39,7 +41,7 @@ __host__ __device__ inline Layout make_layout(int D, int64_t W, int64_t E) {
   L.Dp = p;
   L.W = W;
   L.E = E;
-  L.Epad = ((E + kAlignEv - 1) / kAlignEv) * kAlignEv + (int64_t)kAlignEv * W + kAlignEv;
+  L.Epad = ((E + kAlignEv - 1) / kAlignEv) * kAlignEv + (int64_t)kWinStride * W + kAlignEv;
   size_t o = 0;
   L.begin = o;    o = align256(o + sizeof(int64_t) * W);
   L.n = o;        o = align256(o + sizeof(int32_t) * W);

@@ -60,7 +60,6 @@ struct Smem {
 // row) and accumulates its gradient terms into the never-read row DP of G.  So the event loop
 // needs no per-event predicate.
 constexpr float kNullT = -2.0f;
-constexpr unsigned kNullMarks = 0xffffffffu;
 
 // Zero the dynamic state (S, Q', gR, gQ) of this lane's column j and its row-j entry of the
 // null column; (re)set the null row.
@@ -129,28 +128,37 @@ struct Log2<1> {
 // R_ij and Q_ij in registers; one reduce-scatter gives every lane the intensity of one event
 // (one rcp and one lg2 per lane per chunk instead of per event); pass 2 broadcasts w = 1/lambda
 // per event (1 shuffle) and accumulates the gradients.  DP <= 4 reduces each event directly.
-// 8 null events (t = kNullT, gap 0, mark 0xFF): chunks past a group's last event are read
-// from here, so every chunk load is unconditional (no predicated loads / default registers).
-__device__ __align__(32) float g_null_t[8] = {kNullT, kNullT, kNullT, kNullT,
-                                              kNullT, kNullT, kNullT, kNullT};
-__device__ __align__(32) float g_null_d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-__device__ __align__(8) uint8_t g_null_m[8] = {0xff, 0xff, 0xff, 0xff, 0xff, 0xff, 0xff, 0xff};
-
 struct Chunk {
   float4 ta, tb, da, db;
   uint2 mm;
 };
 
+// Chunk loads use 32-bit event offsets from the window base.  Offsets past the window are
+// clamped to its null chunk (the 8 null events the packer stores after every window), so
+// every load is unconditional.
 __device__ __forceinline__ void load_chunk(Chunk& c, const float* t32, const float* dtp,
-                                           const uint8_t* mk, int64_t off, bool real) {
-  const float4* tp = reinterpret_cast<const float4*>(real ? t32 + off : g_null_t);
-  const float4* dp = reinterpret_cast<const float4*>(real ? dtp + off : g_null_d);
-  const uint2* mp = reinterpret_cast<const uint2*>(real ? mk + off : g_null_m);
+                                           const uint8_t* mk, int off) {
+  const float4* tp = reinterpret_cast<const float4*>(t32 + off);
+  const float4* dp = reinterpret_cast<const float4*>(dtp + off);
   c.ta = __ldg(tp);
   c.tb = __ldg(tp + 1);
   c.da = __ldg(dp);
   c.db = __ldg(dp + 1);
-  c.mm = __ldg(mp);
+  c.mm = __ldg(reinterpret_cast<const uint2*>(mk + off));
+}
+
+// (x == y) ? a : b as one compare + one FSEL (keeps the compiler from SEL + I2FP sequences)
+__device__ __forceinline__ float fsel_eqf(float x, float y, float a, float b) {
+  float r;
+  asm("{\n\t.reg .pred p;\n\tsetp.eq.f32 p, %1, %2;\n\tselp.f32 %0, %3, %4, p;\n\t}"
+      : "=f"(r) : "f"(x), "f"(y), "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fsel_eqi(int x, int y, float a, float b) {
+  float r;
+  asm("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %1, %2;\n\tselp.f32 %0, %3, %4, p;\n\t}"
+      : "=f"(r) : "r"(x), "r"(y), "f"(a), "f"(b));
+  return r;
 }
 
 // One chunk of 8 events (see event_loop).
@@ -161,7 +169,12 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
                                               float& last, float& gth, double& lsum) {
   constexpr int RS = DP + 1;
   constexpr int LG = Log2<DP>::v;
-  const int colb = j * RS;
+  // per-lane bases: row i of column j at rowA + i*RS, column i of row j at colA + i
+  const float2* rowA = A + j;
+  float2* rowS = SQ + j;
+  const float2* colA = A + j * RS;
+  float2* colS = SQ + j * RS;
+  float2* rowG = Gs + j;
   float pv[8], Rv[8], Qv[8];
   float lacc = 0.0f;
 #pragma unroll
@@ -171,19 +184,18 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     const float dc = s == 0 ? ck.da.x : s == 1 ? ck.da.y : s == 2 ? ck.da.z : s == 3 ? ck.da.w
                    : s == 4 ? ck.db.x : s == 5 ? ck.db.y : s == 6 ? ck.db.z : ck.db.w;
     const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
-    const int i = min((int)((word >> (8 * (s & 3))) & 0xffu), DP);
-    const float2 ar = A[i * RS + j];
-    const float2 sr = SQ[i * RS + j];
-    const float bc = A[colb + i].y;
-    const float2 sc = SQ[colb + i];
+    const int i = (int)__byte_perm(word, 0u, 0x4440u | (unsigned)(s & 3));   // mark (null: DP)
+    const float2 ar = rowA[i * RS];
+    const float2 sr = rowS[i * RS];
+    const float bc = colA[i].y;
+    const float2 sc = colS[i];
     const float dr = t - last;
     const float er = ex2f(ar.y * (dr * -kLog2e));
     const float ec = ex2f(bc * (dc * -kLog2e));
-    const float R = fmaf(er, sr.x, (dr == 0.0f) ? -1.0f : 0.0f);  // strict T_j^k < t
-    const bool own = i == j;
-    const float p = fmaf(ar.x, R, own ? th : 0.0f);     // theta_i enters through lane i
-    SQ[colb + i] = make_float2(fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
-    last = own ? t : last;
+    const float R = fmaf(er, sr.x, fsel_eqf(dr, 0.0f, -1.0f, 0.0f));  // strict T_j^k < t
+    const float p = fmaf(ar.x, R, fsel_eqi(i, j, th, 0.0f));   // theta_i enters through lane i
+    colS[i] = make_float2(fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
+    last = fsel_eqi(i, j, t, last);
     if constexpr (DP >= 8) {
       pv[s] = p;
       if (GRAD) {
@@ -194,11 +206,11 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
       const float lam = group_sum<DP>(p);
       if (GRAD) {
         const float w = rcpf(lam);
-        float2 gg = Gs[i * DP + j];
+        float2 gg = rowG[i * DP];
         gg.x = fmaf(R, w, gg.x);
         gg.y = fmaf(er * fmaf(dr, sr.x, sr.y), w, gg.y);
-        Gs[i * DP + j] = gg;
-        gth += own ? w : 0.0f;
+        rowG[i * DP] = gg;
+        gth += fsel_eqi(i, j, w, 0.0f);
       }
       lacc += (j == 0) ? lg2f(lam) : 0.0f;
     }
@@ -213,12 +225,12 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
       for (int s = 0; s < 8; s++) {
         const float ws = __shfl_sync(kFull, w, gbase + (s << (LG - 3)));
         const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
-        const int i = min((int)((word >> (8 * (s & 3))) & 0xffu), DP);
-        float2 gg = Gs[i * DP + j];
+        const int i = (int)__byte_perm(word, 0u, 0x4440u | (unsigned)(s & 3));
+        float2 gg = rowG[i * DP];
         gg.x = fmaf(Rv[s], ws, gg.x);
         gg.y = fmaf(Qv[s], ws, gg.y);
-        Gs[i * DP + j] = gg;
-        gth += (i == j) ? ws : 0.0f;
+        rowG[i * DP] = gg;
+        gth += fsel_eqi(i, j, ws, 0.0f);
       }
     }
   }
@@ -242,13 +254,18 @@ __device__ __forceinline__ void event_loop(const float2* __restrict__ A, float2*
   last = last0;
   gth = 0.0f;
   lsum = 0.0;
+  // window base pointers; chunk offsets are clamped to the window's null chunk at npad
+  const float* tw = t32 + beg;
+  const float* dw = dtp + beg;
+  const uint8_t* mw = mk + beg;
+  const int npad = (n + 7) & ~7;
   Chunk c0, c1;
-  load_chunk(c0, t32, dtp, mk, beg, n > 0);
+  load_chunk(c0, tw, dw, mw, 0 < n ? 0 : npad);
   for (int base = 0; base < nmax; base += 16) {
-    load_chunk(c1, t32, dtp, mk, beg + base + 8, base + 8 < n);
+    load_chunk(c1, tw, dw, mw, min(base + 8, npad));
     process_chunk<DP, GRAD>(c0, A, SQ, Gs, j, gbase, th, last, gth, lsum);
     if (base + 8 >= nmax) break;
-    load_chunk(c0, t32, dtp, mk, beg + base + 16, base + 16 < n);
+    load_chunk(c0, tw, dw, mw, min(base + 16, npad));
     process_chunk<DP, GRAD>(c1, A, SQ, Gs, j, gbase, th, last, gth, lsum);
   }
 }

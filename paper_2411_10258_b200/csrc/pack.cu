@@ -36,7 +36,7 @@ k_pack_events(int D, int Dp, int mode, double lo, double hi, int nudge, int64_t 
   if (n < 0) { st |= MDHP_ST_OUT_OF_RANGE; n = 0; }
   if (!(T > 0.0) || !isfinite(T)) st |= MDHP_ST_BAD_T;
   if (n == 0) st |= MDHP_ST_EMPTY;
-  const int64_t beg = round8(a) + (int64_t)kAlignEv * w;
+  const int64_t beg = round8(a) + (int64_t)kWinStride * w;
 
   double mn = INFINITY, mx = -INFINITY;
   if (mode == MDHP_TIME_EQ6) {
@@ -134,11 +134,11 @@ k_pack_events(int D, int Dp, int mode, double lo, double hi, int nudge, int64_t 
     }
     __syncwarp();
   }
-  const int64_t npad = round8(n);
-  for (int64_t k = n + lane; k < npad; k += 32) {   // null events (eval.cuh: kNullT)
+  const int64_t npad = round8(n) + 8;   // padding to 8 + one null chunk (eval.cuh: kNullT)
+  for (int64_t k = n + lane; k < npad; k += 32) {
     o_t32[beg + k] = -2.0f;
     o_dtp[beg + k] = 0.0f;
-    o_mark[beg + k] = 0xFF;
+    o_mark[beg + k] = (uint8_t)Dp;
   }
   if (lane < Dp) {
     const int c = lane < D ? s_cnt[wp][lane] : 0;

@@ -37,7 +37,7 @@ __host__ __device__ inline SeqLayout make_seq_layout(int D, int64_t N, int ce) {
   L.Dp = p;
   L.N = N;
   L.C = N > 0 ? (N + ce - 1) / ce : 0;
-  L.Epad = ((N + 7) / 8) * 8 + 8 * L.C + 8;
+  L.Epad = ((N + 7) / 8) * 8 + 16 * L.C + 8;
   size_t o = 0;
   L.cstart = o; o = align256(o + sizeof(int64_t) * (L.C + 1));
   L.cbeg = o;   o = align256(o + sizeof(int64_t) * L.C);
@@ -75,7 +75,7 @@ __global__ void k_seq_bounds(int64_t N, int64_t C, int ce, const double* __restr
   if (b > N) b = N;
   while (b > 0 && b < N && t[b] == t[b - 1]) b++;   // never split a tie group
   cstart[c] = b;
-  if (c < C) cbeg[c] = ((b + 7) & ~int64_t(7)) + 8 * c;
+  if (c < C) cbeg[c] = ((b + 7) & ~int64_t(7)) + 16 * c;
 }
 
 // One warp per chunk: relative times, same-mark gaps, validation, per-chunk counts/first times.
@@ -136,11 +136,11 @@ k_seq_events(int D, int Dp, int64_t N, int64_t C, double T, const double* __rest
     }
     __syncwarp();
   }
-  const int64_t npad = (n + 7) & ~int64_t(7);
+  const int64_t npad = ((n + 7) & ~int64_t(7)) + 8;   // padding + one null chunk
   for (int64_t k = n + lane; k < npad; k += 32) {
     o_t[beg + k] = kNullT;
     o_d[beg + k] = 0.0f;
-    o_m[beg + k] = 0xFF;
+    o_m[beg + k] = (uint8_t)Dp;
   }
   if (lane < Dp) {
     ccnt[c * Dp + lane] = lane < D ? s_cnt[wp][lane] : 0;
