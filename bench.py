@@ -349,9 +349,27 @@ def main():
     # ---- roofline of the dominant kernel (k_fit): algorithmic MUFU ops / its CUDA-event time
     mufu_per_ev = 2 * D + 2
     achieved = ev_it_step * mufu_per_ev / (fit_avg / 1e3) / 1e9
+    # DRAM traffic of this launch from the committed ncu capture of the same launch config
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "r01_k_fit_traffic_cfg5.json")
+    if os.path.exists(tf):
+        tj = json.load(open(tf))
+        if tj["windows"] == W and tj["events"] == E and tj["evaluations_per_window"] == args.iters + 1:
+            traffic = tj["traffic_bytes_per_launch"]
+    # shared-memory roofline of the same kernel: algorithmic smem bytes per event-evaluation
+    # (row {alpha,beta}+{S,Q'} 16 B, column beta+{S,Q'} 12 B + {S,Q'} store 8 B, gradient RMW 16 B,
+    # per lane, Dp lanes) against 128 B/clk/SM
+    Dp = 1 << (D - 1).bit_length()
+    smem_bytes = ev_it_step * 52 * Dp
+    smem_peak = 148 * 128 * 1.965   # GB/s at clocks.max.sm
     roof = {"bound": "alu", "achieved": achieved, "peak": MUFU_PEAK_GOPS, "unit": "Gop/s (MUFU)",
-            "frac": achieved / MUFU_PEAK_GOPS, "traffic": None, "kernel": "k_fit<16>",
+            "frac": achieved / MUFU_PEAK_GOPS, "traffic": traffic, "kernel": f"k_fit<{Dp}>",
             "per_unit": f"{mufu_per_ev} MUFU ops per event-iteration (2D ex2 + lg2 + rcp)",
+            "peak_basis": "148 SMs x 16 MUFU/clk x 1.965 GHz (guide unit count x clocks.max.sm); "
+                          "measured ex2 rate 4618 Gop/s (profiles/r01_ubench_b200.txt)",
+            "smem": {"achieved_GBps": smem_bytes / (fit_avg / 1e3) / 1e9, "peak_GBps": smem_peak,
+                     "frac": smem_bytes / (fit_avg / 1e3) / 1e9 / smem_peak,
+                     "per_unit": f"{52 * Dp} B shared-memory traffic per event-iteration"},
             "fit_ms_avg": fit_avg, "fit_share_of_step": fit_avg / (ms / args.steps)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
