@@ -264,7 +264,8 @@ __device__ __forceinline__ void event_loop(const float2* __restrict__ A, float2*
   for (int base = 0; base < nmax; base += 16) {
     load_chunk(c1, tw, dw, mw, min(base + 8, npad));
     process_chunk<DP, GRAD>(c0, A, SQ, Gs, j, gbase, th, last, gth, lsum);
-    if (base + 8 >= nmax) break;
+    // no early exit: a second chunk past nmax is all null events (exact no-ops), and one basic
+    // block per iteration lets ptxas overlap chunk c's reduction with chunk c+1's row reads
     load_chunk(c0, tw, dw, mw, min(base + 16, npad));
     process_chunk<DP, GRAD>(c1, A, SQ, Gs, j, gbase, th, last, gth, lsum);
   }

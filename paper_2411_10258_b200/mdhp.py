@@ -76,7 +76,7 @@ def lib() -> ctypes.CDLL:
     """Load libmdhp.so (building it with nvcc if stale).  Raises if it cannot be loaded."""
     global _lib
     if _lib is None:
-        path = _build.LIB
+        path = os.environ.get("MDHP_LIB") or _build.LIB   # MDHP_LIB: A/B experiments only
         if not os.path.exists(path):
             path = _build.build()
         L = ctypes.CDLL(path)
