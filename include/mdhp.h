@@ -143,6 +143,18 @@ int mdhp_loglik_grad(const mdhp_pack_desc* desc, const void* packed,
                      double* loglik, float* g_theta, float* g_alpha, float* g_beta,
                      const int32_t* win_status, void* stream);
 
+/*
+ * mdhp_loglik_dense — ABLATION: lnL of Eq.(5) evaluated the way the
+ * paper's Algorithms 1-3 do, i.e. by summing over ALL causal pairs (O(N^2)
+ * exponentials per window instead of the recurrence's 2 D N), in the Eq.(5)-correct form
+ * (causal mask, Part3 with "-1"; R4/R5).  Same arguments and layout as
+ * mdhp_loglik_grad without gradients.  Not used by mdhp_fit; it exists to measure the paper's
+ * method on the same GPU and as an independent GPU cross-check.  Asynchronous.
+ */
+int mdhp_loglik_dense(const mdhp_pack_desc* desc, const void* packed, const float* theta,
+                      const float* alpha, const float* beta, double* loglik,
+                      const int32_t* win_status, void* stream);
+
 /* ---------------------------------------------------------------- fit */
 #define MDHP_OPT_GD    0
 #define MDHP_OPT_ADAM  1       /* torch.optim.Adam semantics (amsgrad off, no weight decay) */

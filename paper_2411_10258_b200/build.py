@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libmdhp.so")
-SOURCES = ["abi.cu", "pack.cu", "fit.cu", "seq.cu"]
+SOURCES = ["abi.cu", "pack.cu", "fit.cu", "seq.cu", "dense.cu"]
 HEADERS = ["common.cuh", "eval.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xlinker", "--no-undefined"]

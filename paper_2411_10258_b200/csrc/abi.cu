@@ -18,6 +18,8 @@ int fit_launch(const Packed& P, const FitCfgDev& cfg, float* th, float* al, floa
                double* lnl, int32_t* iters, int32_t* status, float* trace, int* counter,
                cudaStream_t st);
 
+int dense_launch(const Packed& P, const float* th, const float* al, const float* be, double* lnl,
+                 const int32_t* status, cudaStream_t st);
 int seq_pack_launch(int D, int64_t N, int ce, double T, const double* t, const int32_t* mark,
                     void* packed, int32_t* status_out, cudaStream_t st);
 int seq_loglik_launch(int D, int64_t N, int ce, double T, const void* pk, const float* th,
@@ -195,6 +197,21 @@ int mdhp_loglik_grad(const mdhp_pack_desc* d, const void* packed, const float* t
                      (cudaStream_t)stream);
   if (rc) return rc;
   return check_cuda("mdhp_loglik_grad");
+}
+
+int mdhp_loglik_dense(const mdhp_pack_desc* d, const void* packed, const float* theta,
+                      const float* alpha, const float* beta, double* loglik,
+                      const int32_t* win_status, void* stream) {
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!packed || !theta || !alpha || !beta || !loglik || !win_status) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  const Layout L = make_layout(d->D, d->n_windows, d->n_events);
+  rc = dense_launch(view(L, packed), theta, alpha, beta, loglik, win_status, (cudaStream_t)stream);
+  if (rc) return rc;
+  return check_cuda("mdhp_loglik_dense");
 }
 
 int mdhp_fit(const mdhp_pack_desc* d, const void* packed, const mdhp_fit_config* cfg, float* theta,

@@ -551,10 +551,9 @@ k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
   if (ctl && ctl->done && grad) return;
   __shared__ double red[1024];
   __shared__ int okflag;
-  __shared__ double s_lnl;
   const int tid = threadIdx.x;
   const int DD = D * D;
-  const int i = tid / D, j = tid % D;
+  const int j = tid % D;
   const bool pair = tid < DD;
   if (tid == 0) okflag = 1;
   __syncthreads();

@@ -87,6 +87,8 @@ def lib() -> ctypes.CDLL:
         L.mdhp_pack_windows.argtypes = [ctypes.POINTER(PackDesc), P, P, P, P, P, ctypes.c_size_t, P, P]
         L.mdhp_loglik_grad.restype = ctypes.c_int
         L.mdhp_loglik_grad.argtypes = [ctypes.POINTER(PackDesc), P, P, P, P, P, P, P, P, P, P]
+        L.mdhp_loglik_dense.restype = ctypes.c_int
+        L.mdhp_loglik_dense.argtypes = [ctypes.POINTER(PackDesc), P, P, P, P, P, P, P]
         L.mdhp_fit.restype = ctypes.c_int
         L.mdhp_fit.argtypes = [ctypes.POINTER(PackDesc), P, ctypes.POINTER(FitConfigC), P, P, P, P, P,
                                P, P, P, P]
@@ -229,6 +231,17 @@ def loglik_grad(pk: Packed, theta, alpha, beta, grads=True, out=None, stream=Non
                                 _ptr(pk.status), _stream(stream))
     _check(rc, "mdhp_loglik_grad")
     return {"lnl": lnl, "g_theta": gt, "g_alpha": ga, "g_beta": gb}
+
+
+def loglik_dense(pk: Packed, theta, alpha, beta, out=None, stream=None):
+    """mdhp_loglik_dense (ablation f3): lnL by the paper's all-pairs method.  -> lnL f64[W]."""
+    for nm, x in (("theta", theta), ("alpha", alpha), ("beta", beta)):
+        _dev(x, torch.float32, nm)
+    lnl = out if out is not None else torch.empty(pk.W, dtype=torch.float64, device=theta.device)
+    rc = lib().mdhp_loglik_dense(ctypes.byref(pk.desc), _ptr(pk.buf), _ptr(theta), _ptr(alpha), _ptr(beta),
+                                 _ptr(lnl), _ptr(pk.status), _stream(stream))
+    _check(rc, "mdhp_loglik_dense")
+    return lnl
 
 
 def fit(pk: Packed, theta, alpha, beta, cfg: FitConfig, opt_state=None, trace=False, stream=None):
