@@ -8,6 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libmdhp.so")
+LIB_DEBUG = os.path.join(LIBDIR, "libmdhp_debug.so")   # -DMDHP_DEBUG: device bounds asserts
 SOURCES = ["abi.cu", "pack.cu", "fit.cu", "seq.cu", "dense.cu"]
 HEADERS = ["common.cuh", "eval.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -21,13 +22,14 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(os.path.dirname(HERE), "include", "mdhp.h")]
     os.makedirs(LIBDIR, exist_ok=True)
-    if force or _stale(LIB, deps):
-        cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB, *srcs]
+    out = LIB_DEBUG if debug else LIB
+    if force or _stale(out, deps):
+        cmd = ["nvcc", *NVCC_FLAGS, *(["-DMDHP_DEBUG"] if debug else []), "-o", out, *srcs]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -35,7 +37,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
         if verbose:
             print(r.stderr)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

@@ -3,8 +3,17 @@
 #pragma once
 #include <cstdint>
 #include <cstddef>
+#include <cassert>
 #include <cuda_runtime.h>
 #include "../../include/mdhp.h"
+
+// Device-side bounds checks, compiled in only for the debug library (build.py debug=True,
+// -DMDHP_DEBUG); the tests run the GPU suites against it (compute-sanitizer is closed here).
+#ifdef MDHP_DEBUG
+#define MDHP_ASSERT(x) assert(x)
+#else
+#define MDHP_ASSERT(x) ((void)0)
+#endif
 
 namespace mdhp {
 

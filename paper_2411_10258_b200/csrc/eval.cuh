@@ -138,6 +138,7 @@ struct Chunk {
 // every load is unconditional.
 __device__ __forceinline__ void load_chunk(Chunk& c, const float* t32, const float* dtp,
                                            const uint8_t* mk, int off) {
+  MDHP_ASSERT(off >= 0 && (off & 7) == 0);
   const float4* tp = reinterpret_cast<const float4*>(t32 + off);
   const float4* dp = reinterpret_cast<const float4*>(dtp + off);
   c.ta = __ldg(tp);
@@ -185,6 +186,7 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
                    : s == 4 ? ck.db.x : s == 5 ? ck.db.y : s == 6 ? ck.db.z : ck.db.w;
     const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
     const int i = (int)__byte_perm(word, 0u, 0x4440u | (unsigned)(s & 3));   // mark (null: DP)
+    MDHP_ASSERT(i >= 0 && i <= DP);
     const float2 ar = rowA[i * RS];
     const float2 sr = rowS[i * RS];
     const float bc = colA[i].y;
@@ -226,6 +228,7 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
         const float ws = __shfl_sync(kFull, w, gbase + (s << (LG - 3)));
         const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
         const int i = (int)__byte_perm(word, 0u, 0x4440u | (unsigned)(s & 3));
+        MDHP_ASSERT(i >= 0 && i <= DP);
         float2 gg = rowG[i * DP];
         gg.x = fmaf(Rv[s], ws, gg.x);
         gg.y = fmaf(Qv[s], ws, gg.y);
@@ -259,6 +262,7 @@ __device__ __forceinline__ void event_loop(const float2* __restrict__ A, float2*
   const float* dw = dtp + beg;
   const uint8_t* mw = mk + beg;
   const int npad = (n + 7) & ~7;
+  MDHP_ASSERT(n >= 0 && nmax >= n);
   Chunk c0, c1;
   load_chunk(c0, tw, dw, mw, 0 < n ? 0 : npad);
   for (int base = 0; base < nmax; base += 16) {

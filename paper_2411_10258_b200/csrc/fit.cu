@@ -222,6 +222,7 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
     if (unit >= nunits) break;
     const int64_t slot = unit * SM::G + c.g;
     const int64_t w = slot < P.W ? P.perm[slot] : 0;
+    MDHP_ASSERT(w >= 0 && w < (P.W > 0 ? P.W : 1));
     const int st0 = slot < P.W ? status[w] : MDHP_ST_INVALID;
     const bool live = slot < P.W && !(st0 & MDHP_ST_INVALID);
     float th = load_params<DP>(A, c, D, w, live, theta, alpha, beta);

@@ -135,6 +135,7 @@ k_pack_events(int D, int Dp, int mode, double lo, double hi, int nudge, int64_t 
     __syncwarp();
   }
   const int64_t npad = round8(n) + 8;   // padding to 8 + one null chunk (eval.cuh: kNullT)
+  MDHP_ASSERT(beg >= 0 && (beg & 7) == 0);
   for (int64_t k = n + lane; k < npad; k += 32) {
     o_t32[beg + k] = -2.0f;
     o_dtp[beg + k] = 0.0f;
@@ -243,6 +244,7 @@ __global__ void k_sort_scatter(int64_t W, const int32_t* __restrict__ nwin,
   if (w >= W) return;
   int b = (status[w] & MDHP_ST_INVALID) ? 0 : min(nwin[w], kSortBuckets - 1);
   int pos = atomicAdd(&cursor[kSortBuckets - 1 - b], 1);
+  MDHP_ASSERT(pos >= 0 && pos < W);
   perm[pos] = (int32_t)w;
 }
 

@@ -92,6 +92,7 @@ k_seq_events(int D, int Dp, int64_t N, int64_t C, double T, const double* __rest
   const int64_t c = (int64_t)blockIdx.x * kSeqWPB + wp;
   if (c >= C) return;
   const int64_t a = cstart[c], z = cstart[c + 1], n = z - a, beg = cbeg[c];
+  MDHP_ASSERT(a >= 0 && z <= N && n >= 0 && (beg & 7) == 0);
   const double tau = a > 0 ? t[a - 1] : 0.0;
   s_last[wp][lane] = 0.0;
   s_first[wp][lane] = 0.0;
@@ -334,6 +335,7 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
     const float t = act ? t32[beg + k] : 0.0f;
     const float dc = act ? dtp[beg + k] : 0.0f;
     const int i = act ? (int)mk[beg + k] : 0;
+    MDHP_ASSERT(i >= 0 && i < DP);
     if (act) {
       const float2 s = SQ[j * RS + i];
       const float e = ex2f(B[j * RS + i] * (dc * -kLog2e));
