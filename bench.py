@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-windows", type=int, default=None)
     ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--shard-seq", action="store_true",
+                    help="cfg4: split ONE sequence over the ranks (f1, strong scaling, NCCL map exchange)")
     return ap.parse_args()
 
 
@@ -56,6 +58,62 @@ WORKLOADS = {
 }
 
 
+def bench_seq_sharded(args, rc, world, rank, dev):
+    """f1: ONE cfg4 sequence (window index 0 of the seeded stream on every rank) split over the
+    ranks; per iteration one all_gather of slice maps and one all_reduce of partial sums (NCCL)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2411_10258_b200 as M
+    from paper_2411_10258_b200 import seqdist
+    from synth import gpu as sgpu
+    D = rc.D
+    b = sgpu.make_batch_gpu(rc, 1, seed=args.seed, first_window=0, device=dev)
+    N = int(b["win_off"][-1])
+    t_h = b["t"].cpu().numpy()
+    lo, hi = seqdist.slice_bounds(t_h, world)[rank]
+    t0 = float(t_h[lo - 1]) if lo > 0 else 0.0
+    cfg = M.FitConfig(max_iters=args.iters, optimizer="adam", lr=0.05, tol_rel=0.0)
+    comm = seqdist.TorchComm() if world > 1 else seqdist.LocalComm(1)
+    th0 = b["theta"][0].clone(); al0 = b["alpha"][0].clone(); be0 = b["beta"][0].clone()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ctx = seqdist.make_slice(D, b["t"][lo:hi].contiguous(), b["mark"][lo:hi].contiguous(), rc.T, t0,
+                                 rank, chunk_events=256, cfg=cfg)
+        p = {"theta": th0.clone(), "alpha": al0.clone(), "beta": be0.clone()}
+        return seqdist.fit([ctx], comm, [p], cfg, n_total=N)[0]
+    for _ in range(args.warmup):
+        o = step()
+    torch.cuda.synchronize()
+    evals = int(o["iters"][0]) + 1
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        o = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    value = N * evals * args.steps / (float(t_max) / 1e3)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": float(t_max) / args.steps,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                          "data": f"synthetic (Ogata-thinned MDHP on GPU, recipe cfg4, seed {args.seed})",
+                          "config": {"workload": f"cfg4 sharded (f1): one sequence of {N} events, D={D}, split "
+                                                 f"over {world} GPU(s); per iteration all_gather of slice maps + "
+                                                 f"all_reduce of partial sums; Adam, {args.iters} iterations",
+                                     "events": N, "lnl": float(o['lnl'][0])}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def bench_seq(args, rc, world, rank, dev):
     """--config cfg4: one long sequence per GPU (replicas at N > 1: the sequence path does not
     shard), fitted by the chunked-scan path (mdhp_seq_fit)."""
@@ -64,6 +122,8 @@ def bench_seq(args, rc, world, rank, dev):
     import paper_2411_10258_b200 as M
     from synth import gpu as sgpu
     D = rc.D
+    if args.shard_seq:
+        return bench_seq_sharded(args, rc, world, rank, dev)
     b = sgpu.make_batch_gpu(rc, 1, seed=args.seed, first_window=rank, device=dev)
     N = int(b["win_off"][-1])
     ps = M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=256)

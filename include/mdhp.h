@@ -218,8 +218,13 @@ int mdhp_fit_host(const mdhp_pack_desc* desc, const double* t_host, const int32_
 typedef struct {
     int32_t D;             /* 1..32                                                         */
     int32_t chunk_events;  /* >= 8; 256 is a good default                                   */
-    int64_t n_events;      /* N >= 0                                                         */
+    int64_t n_events;      /* N >= 0 (of this slice, see f1 below)                          */
     double  T;             /* horizon T_span > 0                                             */
+    double  t0;            /* slice base: 0 for a whole sequence; for rank r > 0 of a sliced */
+                           /* sequence, the time of the previous slice's last event          */
+    int32_t has_history;   /* 0: empty history at t0 (whole sequence / rank 0); 1: the state */
+                           /* carried in from earlier slices applies (rank > 0)              */
+    int32_t reserved;      /* 0                                                              */
 } mdhp_seq_desc;
 
 size_t mdhp_seq_packed_bytes(const mdhp_seq_desc* desc);
@@ -242,6 +247,41 @@ int mdhp_seq_loglik_grad(const mdhp_seq_desc* desc, const void* packed, const fl
 int mdhp_seq_fit(const mdhp_seq_desc* desc, const void* packed, const mdhp_fit_config* cfg,
                  float* theta, float* alpha, float* beta, float* opt_state, double* loglik,
                  int32_t* iters, int32_t* status, float* lnl_trace, void* stream);
+
+/* ---------------------------------------------------------------- f1: one sequence over GPUs
+ * SURVEY 8(f) f1.  Rank r holds a contiguous slice of the sequence (packed with t0 = previous
+ * slice's last event and has_history = r > 0).  Per evaluation:
+ *   1. mdhp_seq_maps   local chunk states + the slice's composite affine map from a zero state
+ *                      (rankmap = {S, Q'} per pair at the slice's last event, rankspan = its span)
+ *   2. all_gather of (rankmap, rankspan) over ranks          [the exchange: 2 D^2 + 1 floats/rank]
+ *   3. mdhp_seq_parts  carried-in state = earlier slices' maps composed in order, then the chunk
+ *                      scan, the event loop and fixed-order sums -> parts (2 D^2 + D + 1 fp64:
+ *                      gR, gQ interleaved, g_theta, sum lg2 lambda) and fin (end state)
+ *   4. all_reduce(sum) of parts; fin of the last rank is the global final state
+ *   5. mdhp_seq_finish epilogue (and with cfg, one step of the DESIGN.md "Fit" loop), identical
+ *                      on every rank.  Stats (counts, u_max, moments, tail) are combined once per
+ *                      fit: mdhp_seq_stats per rank -> all_gather -> mdhp_seq_stats_combine.
+ * Exact decomposition: the same lnL and gradients as the single-GPU path up to fp32 rounding.
+ * `work` is a caller-owned device buffer of mdhp_seq_work_bytes() bytes, initialised with
+ * mdhp_seq_work_init (cfg NULL for evaluation only).  All calls are asynchronous.            */
+size_t mdhp_seq_work_bytes(const mdhp_seq_desc* desc);
+int mdhp_seq_work_init(const mdhp_seq_desc* desc, void* work, const mdhp_fit_config* cfg,
+                       void* stream);
+int mdhp_seq_maps(const mdhp_seq_desc* desc, const void* packed, const float* beta, void* work,
+                  float* rankmap, float* rankspan, int32_t fit, void* stream);
+int mdhp_seq_parts(const mdhp_seq_desc* desc, const void* packed, const float* theta,
+                   const float* alpha, const float* beta, const float* maps, const float* spans,
+                   int32_t rank, void* work, double* parts, float* fin, int32_t grad, int32_t fit,
+                   void* stream);
+int mdhp_seq_stats(const mdhp_seq_desc* desc, const void* packed, double* stats, void* stream);
+int mdhp_seq_stats_combine(int32_t D, int32_t R, const double* gathered, double* combined,
+                           void* stream);
+int mdhp_seq_finish(const mdhp_seq_desc* desc, int64_t n_events_total, const double* stats,
+                    const double* parts, const float* fin, float* theta, float* alpha, float* beta,
+                    double* loglik, float* g_theta, float* g_alpha, float* g_beta,
+                    const mdhp_fit_config* cfg, void* work, float* opt_state, float* lnl_trace,
+                    int32_t* status, int32_t* iters, int32_t final_eval, const void* packed,
+                    void* stream);
 
 /* Byte offsets of the packed sections (introspection for tests/tools), in this order:
  * [0] begin i64[W]  [1] n i32[W]  [2] T32 f32[W]  [3] perm i32[W]  [4] t32 f32[Epad]

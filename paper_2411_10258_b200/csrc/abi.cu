@@ -20,8 +20,24 @@ int fit_launch(const Packed& P, const FitCfgDev& cfg, float* th, float* al, floa
 
 int dense_launch(const Packed& P, const float* th, const float* al, const float* be, double* lnl,
                  const int32_t* status, cudaStream_t st);
-int seq_pack_launch(int D, int64_t N, int ce, double T, const double* t, const int32_t* mark,
-                    void* packed, int32_t* status_out, cudaStream_t st);
+int seq_pack_launch(int D, int64_t N, int ce, double T, double t0, const double* t,
+                    const int32_t* mark, void* packed, int32_t* status_out, cudaStream_t st);
+size_t seq_work_bytes_slice(int D, int64_t N, int ce);
+int seq_slice_init_launch(int D, int64_t N, int ce, void* work, const FitCfgDev* cfg, cudaStream_t st);
+int seq_maps_launch(int D, int64_t N, int ce, const void* pk, const float* be, void* work,
+                    float2* rankmap, float* rankspan, int fit, cudaStream_t st);
+int seq_parts_launch(int D, int64_t N, int ce, const void* pk, const float* th, const float* al,
+                     const float* be, const float2* maps, const float* spans, int rank,
+                     int has_history, void* work, double* parts, float2* fin, int grad, int fit,
+                     cudaStream_t st);
+int seq_local_stats_launch(int D, int64_t N, int ce, const void* pk, double* stats, cudaStream_t st);
+int seq_combine_stats_launch(int D, int R, const double* gathered, double* combined, cudaStream_t st);
+int seq_finish_launch(int D, int64_t N_total, int ce, int64_t N_slice, double T,
+                      const double* stats, const double* parts, const float2* fin, float* th,
+                      float* al, float* be, double* lnl, float* gt, float* ga, float* gb,
+                      const FitCfgDev* cfg, void* work, float* opt, float* trace, int32_t* status,
+                      int32_t* iters, int final_eval, const int32_t* pstatus, cudaStream_t st);
+size_t seq_status_offset(int D, int64_t N, int ce);
 int seq_loglik_launch(int D, int64_t N, int ce, double T, const void* pk, const float* th,
                       const float* al, const float* be, double* lnl, float* gt, float* ga,
                       float* gb, cudaStream_t st);
@@ -88,8 +104,9 @@ static int check_seq(const mdhp_seq_desc* d) {
     set_error("bad sequence dims (D=%d, N=%lld)", d->D, (long long)d->n_events);
     return MDHP_EDIM;
   }
-  if (d->chunk_events < 8 || !(d->T > 0.0)) {
-    set_error("chunk_events must be >= 8 and T > 0");
+  if (d->chunk_events < 8 || !(d->T > 0.0) || !(d->t0 >= 0.0) || d->has_history < 0 ||
+      d->has_history > 1) {
+    set_error("chunk_events must be >= 8, T > 0, t0 >= 0, has_history 0/1");
     return MDHP_EINVAL;
   }
   return MDHP_OK;
@@ -283,7 +300,7 @@ int mdhp_seq_pack(const mdhp_seq_desc* d, const double* t, const int32_t* mark, 
     set_error("packed buffer too small: %zu < %zu", packed_bytes, need);
     return MDHP_ESIZE;
   }
-  rc = seq_pack_launch(d->D, d->n_events, d->chunk_events, d->T, t, mark, packed, status,
+  rc = seq_pack_launch(d->D, d->n_events, d->chunk_events, d->T, d->t0, t, mark, packed, status,
                        (cudaStream_t)stream);
   if (rc) {
     set_error("mdhp_seq_pack: CUDA error");
@@ -333,6 +350,105 @@ int mdhp_seq_fit(const mdhp_seq_desc* d, const void* packed, const mdhp_fit_conf
     return rc;
   }
   return check_cuda("mdhp_seq_fit");
+}
+
+size_t mdhp_seq_work_bytes(const mdhp_seq_desc* d) {
+  if (check_seq(d) != MDHP_OK) return 0;
+  return seq_work_bytes_slice(d->D, d->n_events, d->chunk_events);
+}
+
+int mdhp_seq_work_init(const mdhp_seq_desc* d, void* work, const mdhp_fit_config* cfg, void* stream) {
+  int rc = check_seq(d);
+  if (rc) return rc;
+  if (cfg && (rc = check_cfg(cfg))) return rc;
+  if (!work) {
+    set_error("work is NULL");
+    return MDHP_EINVAL;
+  }
+  FitCfgDev c;
+  if (cfg) c = to_dev(cfg);
+  rc = seq_slice_init_launch(d->D, d->n_events, d->chunk_events, work, cfg ? &c : nullptr,
+                             (cudaStream_t)stream);
+  if (rc) set_error("mdhp_seq_work_init: CUDA error");
+  return rc;
+}
+
+int mdhp_seq_maps(const mdhp_seq_desc* d, const void* packed, const float* beta, void* work,
+                  float* rankmap, float* rankspan, int32_t fit, void* stream) {
+  int rc = check_seq(d);
+  if (rc) return rc;
+  if (!packed || !beta || !work || !rankmap || !rankspan) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  rc = seq_maps_launch(d->D, d->n_events, d->chunk_events, packed, beta, work,
+                       reinterpret_cast<float2*>(rankmap), rankspan, fit, (cudaStream_t)stream);
+  if (rc) set_error("mdhp_seq_maps: CUDA error");
+  return rc;
+}
+
+int mdhp_seq_parts(const mdhp_seq_desc* d, const void* packed, const float* theta,
+                   const float* alpha, const float* beta, const float* maps, const float* spans,
+                   int32_t rank, void* work, double* parts, float* fin, int32_t grad, int32_t fit,
+                   void* stream) {
+  int rc = check_seq(d);
+  if (rc) return rc;
+  if (!packed || !theta || !alpha || !beta || !work || !parts || !fin || rank < 0 ||
+      (rank > 0 && (!maps || !spans))) {
+    set_error("bad argument");
+    return MDHP_EINVAL;
+  }
+  rc = seq_parts_launch(d->D, d->n_events, d->chunk_events, packed, theta, alpha, beta,
+                        reinterpret_cast<const float2*>(maps), spans, rank, d->has_history, work,
+                        parts, reinterpret_cast<float2*>(fin), grad, fit, (cudaStream_t)stream);
+  if (rc) set_error("mdhp_seq_parts: CUDA error");
+  return rc;
+}
+
+int mdhp_seq_stats(const mdhp_seq_desc* d, const void* packed, double* stats, void* stream) {
+  int rc = check_seq(d);
+  if (rc) return rc;
+  if (!packed || !stats) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  return seq_local_stats_launch(d->D, d->n_events, d->chunk_events, packed, stats,
+                                (cudaStream_t)stream);
+}
+
+int mdhp_seq_stats_combine(int32_t D, int32_t R, const double* gathered, double* combined,
+                           void* stream) {
+  if (D < 1 || D > 32 || R < 1 || !gathered || !combined) {
+    set_error("bad argument");
+    return MDHP_EINVAL;
+  }
+  return seq_combine_stats_launch(D, R, gathered, combined, (cudaStream_t)stream);
+}
+
+int mdhp_seq_finish(const mdhp_seq_desc* d, int64_t n_total, const double* stats,
+                    const double* parts, const float* fin, float* theta, float* alpha, float* beta,
+                    double* loglik, float* g_theta, float* g_alpha, float* g_beta,
+                    const mdhp_fit_config* cfg, void* work, float* opt_state, float* lnl_trace,
+                    int32_t* status, int32_t* iters, int32_t final_eval, const void* packed,
+                    void* stream) {
+  int rc = check_seq(d);
+  if (rc) return rc;
+  if (cfg && (rc = check_cfg(cfg))) return rc;
+  if (!stats || !parts || !fin || !theta || !alpha || !beta || !loglik || !work || !packed ||
+      (cfg && (!status || !iters))) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  FitCfgDev c;
+  if (cfg) c = to_dev(cfg);
+  const int32_t* pst = reinterpret_cast<const int32_t*>(
+      static_cast<const char*>(packed) + seq_status_offset(d->D, d->n_events, d->chunk_events));
+  rc = seq_finish_launch(d->D, n_total, d->chunk_events, d->n_events, d->T, stats, parts,
+                         reinterpret_cast<const float2*>(fin), theta, alpha, beta, loglik, g_theta,
+                         g_alpha, g_beta, cfg ? &c : nullptr, work, opt_state, lnl_trace, status,
+                         iters, final_eval, pst, (cudaStream_t)stream);
+  if (rc) set_error("mdhp_seq_finish: CUDA error");
+  return rc;
 }
 
 int mdhp_fit_host(const mdhp_pack_desc* d, const double* t_h, const int32_t* mark_h,

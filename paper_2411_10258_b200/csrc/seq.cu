@@ -80,7 +80,7 @@ __global__ void k_seq_bounds(int64_t N, int64_t C, int ce, const double* __restr
 
 // One warp per chunk: relative times, same-mark gaps, validation, per-chunk counts/first times.
 __global__ void __launch_bounds__(kSeqWPB * 32)
-k_seq_events(int D, int Dp, int64_t N, int64_t C, double T, const double* __restrict__ t,
+k_seq_events(int D, int Dp, int64_t N, int64_t C, double T, double t0, const double* __restrict__ t,
              const int32_t* __restrict__ mark, const int64_t* __restrict__ cstart,
              const int64_t* __restrict__ cbeg, float* __restrict__ cspan, float* __restrict__ o_t,
              float* __restrict__ o_d, uint8_t* __restrict__ o_m, int32_t* __restrict__ ccnt,
@@ -93,7 +93,7 @@ k_seq_events(int D, int Dp, int64_t N, int64_t C, double T, const double* __rest
   if (c >= C) return;
   const int64_t a = cstart[c], z = cstart[c + 1], n = z - a, beg = cbeg[c];
   MDHP_ASSERT(a >= 0 && z <= N && n >= 0 && (beg & 7) == 0);
-  const double tau = a > 0 ? t[a - 1] : 0.0;
+  const double tau = a > 0 ? t[a - 1] : t0;   // chunk base: previous event (or the slice base)
   s_last[wp][lane] = 0.0;
   s_first[wp][lane] = 0.0;
   s_cnt[wp][lane] = 0;
@@ -380,7 +380,9 @@ __device__ __forceinline__ AffMap compose(const AffMap& m1, const AffMap& m2) {
 __global__ void __launch_bounds__(kScanSeg)
 k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __restrict__ beta,
            const float2* __restrict__ loc, float2* __restrict__ carry, float2* __restrict__ fin,
-           const int* __restrict__ ctl) {
+           const int* __restrict__ ctl, const float2* __restrict__ maps,
+           const float* __restrict__ spans, int rank, float2* __restrict__ rankmap,
+           float* __restrict__ rankspan, int maps_only) {
   if (ctl && ctl[0]) return;
   __shared__ AffMap sm[kScanSeg];
   const int p = blockIdx.x, s = threadIdx.x;
@@ -405,9 +407,27 @@ k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __res
     sm[s] = m;
     __syncthreads();
   }
-  // state entering segment s = (inclusive map of segment s-1) applied to the zero state
-  float2 x = s > 0 ? make_float2(sm[s - 1].Sb, sm[s - 1].Qb) : make_float2(0.0f, 0.0f);
-  if (s == kScanSeg - 1) fin[p] = make_float2(m.Sb, m.Qb);
+  // state carried into this slice (f1, multi-GPU): the earlier slices' maps composed in order
+  float2 x0 = make_float2(0.0f, 0.0f);
+  if (maps) {
+    for (int r = 0; r < rank; r++) {
+      const float L = spans[r];
+      const float2 l = maps[(size_t)r * DD + p];
+      const float e = ex2f(b * (L * -kLog2e));
+      x0 = make_float2(fmaf(e, x0.x, l.x), fmaf(e, fmaf(L, x0.x, x0.y), l.y));
+    }
+  }
+  auto apply = [&](const AffMap& M, float2 x) {
+    return make_float2(fmaf(M.E, x.x, M.Sb), fmaf(M.E, fmaf(M.L, x.x, x.y), M.Qb));
+  };
+  if (s == kScanSeg - 1) {
+    fin[p] = apply(m, x0);
+    if (rankmap) rankmap[p] = make_float2(m.Sb, m.Qb);
+    if (rankspan && p == 0) rankspan[0] = m.L;
+  }
+  if (maps_only) return;
+  // state entering segment s = (inclusive map of segment s-1) applied to the carried-in state
+  float2 x = s > 0 ? apply(sm[s - 1], x0) : x0;
   for (int64_t c = c0; c < c1; c++) {
     carry[c * DD + p] = x;
     const float L = cspan[c];
@@ -425,7 +445,7 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
            const uint8_t* __restrict__ mk, const float* __restrict__ theta,
            const float* __restrict__ alpha, const float* __restrict__ beta,
            const float2* __restrict__ carry, float2* __restrict__ gpart, float* __restrict__ gthp,
-           double* __restrict__ lsp, int grad, const int* __restrict__ ctl) {
+           double* __restrict__ lsp, int grad, const int* __restrict__ ctl, int has_history) {
   if (ctl && ctl[0] == 1 && grad) return;
   extern __shared__ __align__(16) unsigned char smem[];
   using SM = Smem<DP>;
@@ -459,7 +479,7 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
   double lsum;
   // chunk 0 starts from an empty history (anchor -1, as a window); later chunks from a state
   // anchored at their base (relative time 0; their events are strictly later, R2/R10)
-  const float last0 = c == 0 ? -1.0f : 0.0f;
+  const float last0 = (c == 0 && !has_history) ? -1.0f : 0.0f;
   if (grad)
     event_loop<DP, true>(A, SQ, Gs, j, gbase, t32, dtp, mk, live ? cbeg[c] : 0, n, nmax, th, last,
                          gth, lsum, last0);
@@ -509,12 +529,14 @@ k_seq_reduce1(int D, int Dp, int64_t C, const float2* __restrict__ gpart,
 
 __global__ void __launch_bounds__(1024)
 k_seq_reduce2(int D, const double* __restrict__ part, float2* __restrict__ gsum,
-              float* __restrict__ gth, double* __restrict__ ls, int grad, const int* __restrict__ ctl) {
+              float* __restrict__ gth, double* __restrict__ ls, int grad, const int* __restrict__ ctl,
+              double* __restrict__ raw) {
   if (ctl && ctl[0] == 1 && grad) return;
   const int DD = D * D, NE = 2 * DD + D + 1;
   for (int e = threadIdx.x; e < NE; e += blockDim.x) {
     double acc = 0.0;
     for (int q = 0; q < kRedBlocks; q++) acc += part[(size_t)q * NE + e];
+    if (raw) raw[e] = acc;   // f1: the slice's exact partial sums, all-reduced across ranks
     if (e < 2 * DD) {
       if (grad) reinterpret_cast<float*>(gsum)[e] = (float)acc;
     } else if (e < 2 * DD + D) {
@@ -709,8 +731,8 @@ k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
 }
 
 // ---------------------------------------------------------------- host side
-int seq_pack_launch(int D, int64_t N, int ce, double T, const double* t, const int32_t* mark,
-                    void* packed, int32_t* status_out, cudaStream_t st) {
+int seq_pack_launch(int D, int64_t N, int ce, double T, double t0, const double* t,
+                    const int32_t* mark, void* packed, int32_t* status_out, cudaStream_t st) {
   const SeqLayout L = make_seq_layout(D, N, ce);
   if (cudaMemsetAsync(at<int32_t>(packed, L.status), 0, sizeof(int32_t), st) != cudaSuccess)
     return MDHP_ECUDA;
@@ -720,7 +742,7 @@ int seq_pack_launch(int D, int64_t N, int ce, double T, const double* t, const i
         N, C, ce, t, at<int64_t>(packed, L.cstart), at<int64_t>(packed, L.cbeg));
     const unsigned blocks = (unsigned)((C + kSeqWPB - 1) / kSeqWPB);
     k_seq_events<<<blocks, kSeqWPB * 32, 0, st>>>(
-        D, L.Dp, N, C, T, t, mark, at<int64_t>(packed, L.cstart), at<int64_t>(packed, L.cbeg),
+        D, L.Dp, N, C, T, t0, t, mark, at<int64_t>(packed, L.cstart), at<int64_t>(packed, L.cbeg),
         at<float>(packed, L.cspan), at<float>(packed, L.t32), at<float>(packed, L.dtp),
         at<uint8_t>(packed, L.mark), at<int32_t>(packed, L.ccnt), at<double>(packed, L.cfirst),
         at<int32_t>(packed, L.status));
@@ -751,51 +773,69 @@ int seq_pack_launch(int D, int64_t N, int ce, double T, const double* t, const i
   return cudaGetLastError() == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
 }
 
+struct SeqDist {   // multi-GPU slice context (f1); all null/zero for a whole sequence
+  const float2* maps = nullptr;
+  const float* spans = nullptr;
+  int rank = 0;
+  int has_history = 0;
+  float2* rankmap = nullptr;
+  float* rankspan = nullptr;
+  int maps_only = 0;
+  int skip_local = 0;
+};
+
 template <int DP>
 static void seq_phases_t(const SeqLayout& L, const void* pk, const float* th, const float* al,
                          const float* be, const SeqWork& w, int grad, const int* ctl,
-                         cudaStream_t st) {
+                         cudaStream_t st, const SeqDist& sd) {
   const int64_t C = L.C;
   if (C == 0) return;
   constexpr int G = 32 / DP;
   const unsigned blk = (unsigned)((C + 4 * G - 1) / (4 * G));
   const size_t lsm = (size_t)4 * G * DP * (DP + 1) * (sizeof(float2) + sizeof(float));
   cudaFuncSetAttribute(k_seq_local<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
-  k_seq_local<DP><<<blk, 128, lsm, st>>>(L.D, C, at<int64_t>(pk, L.cstart), at<int64_t>(pk, L.cbeg),
-                                       at<float>(pk, L.cspan), at<float>(pk, L.t32),
-                                       at<float>(pk, L.dtp), at<uint8_t>(pk, L.mark), be, w.loc,
-                                       grad ? ctl : nullptr);
+  if (!sd.skip_local) {
+    k_seq_local<DP><<<blk, 128, lsm, st>>>(L.D, C, at<int64_t>(pk, L.cstart), at<int64_t>(pk, L.cbeg),
+                                         at<float>(pk, L.cspan), at<float>(pk, L.t32),
+                                         at<float>(pk, L.dtp), at<uint8_t>(pk, L.mark), be, w.loc,
+                                         grad ? ctl : nullptr);
+    count_launch();
+  }
   k_seq_scan<<<L.D * L.D, kScanSeg, 0, st>>>(L.D, C, at<float>(pk, L.cspan), be, w.loc, w.carry,
-                                             w.fin, grad ? ctl : nullptr);
+                                             w.fin, grad ? ctl : nullptr, sd.maps, sd.spans,
+                                             sd.rank, sd.rankmap, sd.rankspan, sd.maps_only);
+  count_launch();
+  if (sd.maps_only) return;
+  const int has_history = sd.has_history;
   using SM = Smem<DP>;
   const size_t smem = 4 * SM::per_warp;
   cudaFuncSetAttribute(k_seq_eval<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_seq_eval<DP><<<blk, 128, smem, st>>>(L.D, C, at<int64_t>(pk, L.cstart), at<int64_t>(pk, L.cbeg),
                                          at<float>(pk, L.t32), at<float>(pk, L.dtp),
                                          at<uint8_t>(pk, L.mark), th, al, be, w.carry, w.gpart,
-                                         w.gthp, w.lsp, grad, ctl);
-  count_launch(3);
+                                         w.gthp, w.lsp, grad, ctl, has_history);
+  count_launch();
 }
 
 static void seq_phases(const SeqLayout& L, const void* pk, const float* th, const float* al,
                        const float* be, const SeqWork& w, int grad, const int* ctl,
-                       cudaStream_t st) {
+                       cudaStream_t st, const SeqDist& sd = SeqDist()) {
   switch (L.Dp) {
-    case 1: seq_phases_t<1>(L, pk, th, al, be, w, grad, ctl, st); break;
-    case 2: seq_phases_t<2>(L, pk, th, al, be, w, grad, ctl, st); break;
-    case 4: seq_phases_t<4>(L, pk, th, al, be, w, grad, ctl, st); break;
-    case 8: seq_phases_t<8>(L, pk, th, al, be, w, grad, ctl, st); break;
-    case 16: seq_phases_t<16>(L, pk, th, al, be, w, grad, ctl, st); break;
-    case 32: seq_phases_t<32>(L, pk, th, al, be, w, grad, ctl, st); break;
+    case 1: seq_phases_t<1>(L, pk, th, al, be, w, grad, ctl, st, sd); break;
+    case 2: seq_phases_t<2>(L, pk, th, al, be, w, grad, ctl, st, sd); break;
+    case 4: seq_phases_t<4>(L, pk, th, al, be, w, grad, ctl, st, sd); break;
+    case 8: seq_phases_t<8>(L, pk, th, al, be, w, grad, ctl, st, sd); break;
+    case 16: seq_phases_t<16>(L, pk, th, al, be, w, grad, ctl, st, sd); break;
+    case 32: seq_phases_t<32>(L, pk, th, al, be, w, grad, ctl, st, sd); break;
   }
 }
 
 static void seq_reduce(const SeqLayout& L, const SeqWork& w, int grad, const int* ctl,
-                       cudaStream_t st) {
+                       cudaStream_t st, double* raw = nullptr) {
   if (L.C == 0) return;
   k_seq_reduce1<<<kRedBlocks, 256, 0, st>>>(L.D, L.Dp, L.C, w.gpart, w.gthp, w.lsp, w.rpart, grad,
                                             ctl);
-  k_seq_reduce2<<<1, 1024, 0, st>>>(L.D, w.rpart, w.gsum, w.gth, w.ls, grad, ctl);
+  k_seq_reduce2<<<1, 1024, 0, st>>>(L.D, w.rpart, w.gsum, w.gth, w.ls, grad, ctl, raw);
   count_launch(2);
 }
 
@@ -877,5 +917,202 @@ int seq_fit_launch(int D, int64_t N, int ce, double T, const void* pk, const Fit
 }
 
 size_t seq_packed_bytes(int D, int64_t N, int ce) { return make_seq_layout(D, N, ce).total; }
+size_t seq_status_offset(int D, int64_t N, int ce) { return make_seq_layout(D, N, ce).status; }
+
+// ---------------------------------------------------------------- f1: one sequence over ranks
+// Stats record of a slice (fp64): [cnt Dp | umax Dp | mom Dp*kMom | tail]; partial sums record:
+// [gR,gQ interleaved 2 D^2 | g_theta D | sum lg2 lambda].
+__host__ __device__ inline int seq_stats_len(int Dp) { return 2 * Dp + Dp * kMom + 1; }
+
+__global__ void k_seq_stats_out(int Dp, const int32_t* __restrict__ cnt, const float* __restrict__ umax,
+                                const float* __restrict__ mom, const float* __restrict__ tail,
+                                double* __restrict__ out) {
+  for (int q = threadIdx.x; q < seq_stats_len(Dp); q += blockDim.x) {
+    double v;
+    if (q < Dp) v = cnt[q];
+    else if (q < 2 * Dp) v = umax[q - Dp];
+    else if (q < 2 * Dp + Dp * kMom) v = mom[q - 2 * Dp];
+    else v = tail[0];
+    out[q] = v;
+  }
+}
+
+// Combine R slices' stats: counts add; u_max = max (= T - the global first event of the mark);
+// moments rescale exactly, sum_k (u_k/U)^p = sum_r (U_r/U)^p m_p^(r); tail = min (the global
+// last event).
+__global__ void k_seq_stats_combine(int Dp, int R, const double* __restrict__ g, double* __restrict__ out) {
+  const int S = seq_stats_len(Dp);
+  for (int q = threadIdx.x; q < S; q += blockDim.x) {
+    double v = 0.0;
+    if (q < Dp) {
+      for (int r = 0; r < R; r++) v += g[(size_t)r * S + q];
+    } else if (q < 2 * Dp) {
+      for (int r = 0; r < R; r++) v = fmax(v, g[(size_t)r * S + q]);
+    } else if (q < 2 * Dp + Dp * kMom) {
+      const int j = (q - 2 * Dp) / kMom, pw = (q - 2 * Dp) % kMom + 1;
+      double U = 0.0;
+      for (int r = 0; r < R; r++) U = fmax(U, g[(size_t)r * S + Dp + j]);
+      for (int r = 0; r < R; r++) {
+        const double Ur = g[(size_t)r * S + Dp + j];
+        if (Ur > 0.0) v += pow(Ur / U, (double)pw) * g[(size_t)r * S + q];
+      }
+    } else {
+      v = INFINITY;
+      for (int r = 0; r < R; r++) v = fmin(v, g[(size_t)r * S + q]);
+    }
+    out[q] = v;
+  }
+}
+
+// Unpack combined stats + reduced partial sums into the finish kernel's inputs (work area).
+__global__ void k_seq_unpack(int D, int Dp, const double* __restrict__ stats,
+                             const double* __restrict__ parts, int32_t* __restrict__ cnt,
+                             float* __restrict__ umax, float* __restrict__ mom, float* __restrict__ tail,
+                             float2* __restrict__ gsum, float* __restrict__ gth, double* __restrict__ ls,
+                             double T) {
+  const int DD = D * D;
+  for (int q = threadIdx.x; q < Dp; q += blockDim.x) {
+    cnt[q] = (int32_t)stats[q];
+    umax[q] = (float)stats[Dp + q];
+  }
+  for (int q = threadIdx.x; q < Dp * kMom; q += blockDim.x) mom[q] = (float)stats[2 * Dp + q];
+  if (threadIdx.x == 0) {
+    tail[0] = (float)stats[2 * Dp + Dp * kMom];
+    tail[1] = (float)T;
+    ls[0] = parts[2 * DD + D];
+  }
+  for (int q = threadIdx.x; q < DD; q += blockDim.x)
+    gsum[q] = make_float2((float)parts[2 * q], (float)parts[2 * q + 1]);
+  for (int q = threadIdx.x; q < D; q += blockDim.x) gth[q] = (float)parts[2 * DD + q];
+}
+
+struct SeqFinishArea {   // finish inputs assembled from the global records
+  int32_t* cnt;
+  float *umax, *mom, *tail, *gth;
+  float2* gsum;
+  double* ls;
+};
+
+static SeqFinishArea finish_area(void* work, int Dp) {
+  // the slice work buffer starts with a head region reserved for these small records
+  char* b = static_cast<char*>(work);
+  SeqFinishArea a;
+  a.cnt = reinterpret_cast<int32_t*>(b);
+  a.umax = reinterpret_cast<float*>(b + 256);
+  a.mom = reinterpret_cast<float*>(b + 512);
+  a.tail = reinterpret_cast<float*>(b + 512 + align256(sizeof(float) * Dp * kMom));
+  a.gth = a.tail + 64;
+  a.ls = reinterpret_cast<double*>(a.gth + 64);
+  a.gsum = reinterpret_cast<float2*>(reinterpret_cast<char*>(a.ls) + 256);
+  return a;
+}
+
+size_t seq_work_bytes_slice(int D, int64_t N, int ce) {
+  const SeqLayout L = make_seq_layout(D, N, ce);
+  const size_t wb = make_seq_work(nullptr, D, L.Dp, L.C).bytes;
+  return wb + 8192 + sizeof(float2) * (size_t)D * D;   // + the head region of finish_area
+}
+
+static SeqWork slice_work(int D, int64_t N, int ce, void* work) {
+  const SeqLayout L = make_seq_layout(D, N, ce);
+  char* base = static_cast<char*>(work) + 8192 + sizeof(float2) * (size_t)D * D;   // after the head
+  return make_seq_work(base, D, L.Dp, L.C);
+}
+
+int seq_slice_init_launch(int D, int64_t N, int ce, void* work, const FitCfgDev* cfg, cudaStream_t st) {
+  const size_t wb = seq_work_bytes_slice(D, N, ce);
+  if (cudaMemsetAsync(work, 0, wb, st) != cudaSuccess) return MDHP_ECUDA;
+  if (cfg) {
+    SeqWork w = slice_work(D, N, ce, work);
+    SeqCtl h{};
+    h.lr_w = cfg->lr;
+    h.done = cfg->max_iters <= 0;
+    if (cudaMemcpyAsync(w.ctl, &h, sizeof(SeqCtl), cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return MDHP_ECUDA;
+  }
+  return MDHP_OK;
+}
+
+int seq_maps_launch(int D, int64_t N, int ce, const void* pk, const float* be, void* work,
+                    float2* rankmap, float* rankspan, int fit, cudaStream_t st) {
+  const SeqLayout L = make_seq_layout(D, N, ce);
+  SeqWork w = slice_work(D, N, ce, work);
+  if (L.C == 0) {
+    cudaMemsetAsync(rankmap, 0, sizeof(float2) * (size_t)D * D, st);
+    cudaMemsetAsync(rankspan, 0, sizeof(float), st);
+    return cudaGetLastError() == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
+  }
+  SeqDist sd;
+  sd.maps_only = 1;
+  sd.rankmap = rankmap;
+  sd.rankspan = rankspan;
+  seq_phases(L, pk, nullptr, nullptr, be, w, fit, fit ? w.ctl : nullptr, st, sd);
+  return cudaGetLastError() == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
+}
+
+int seq_parts_launch(int D, int64_t N, int ce, const void* pk, const float* th, const float* al,
+                     const float* be, const float2* maps, const float* spans, int rank,
+                     int has_history, void* work, double* parts, float2* fin, int grad, int fit,
+                     cudaStream_t st) {
+  const SeqLayout L = make_seq_layout(D, N, ce);
+  SeqWork w = slice_work(D, N, ce, work);
+  const size_t DD = (size_t)D * D;
+  if (L.C == 0) {
+    // empty slice: no partial sums; its end state is the carried-in state (maps of earlier ranks)
+    cudaMemsetAsync(parts, 0, sizeof(double) * (2 * DD + D + 1), st);
+    k_seq_scan<<<D * D, kScanSeg, 0, st>>>(D, 0, nullptr, be, nullptr, nullptr, fin, nullptr, maps,
+                                           spans, rank, nullptr, nullptr, 1);
+    count_launch();
+    return cudaGetLastError() == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
+  }
+  SeqDist sd;
+  sd.maps = maps;
+  sd.spans = spans;
+  sd.rank = rank;
+  sd.has_history = has_history;
+  sd.skip_local = 1;   // the local states of mdhp_seq_maps (same work, same beta) are reused
+  seq_phases(L, pk, th, al, be, w, grad, fit ? w.ctl : nullptr, st, sd);
+  seq_reduce(L, w, grad, fit ? w.ctl : nullptr, st, parts);
+  cudaMemcpyAsync(fin, w.fin, sizeof(float2) * DD, cudaMemcpyDeviceToDevice, st);
+  return cudaGetLastError() == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
+}
+
+int seq_local_stats_launch(int D, int64_t N, int ce, const void* pk, double* stats, cudaStream_t st) {
+  const SeqLayout L = make_seq_layout(D, N, ce);
+  k_seq_stats_out<<<1, 256, 0, st>>>(L.Dp, at<int32_t>(pk, L.cnt), at<float>(pk, L.umax),
+                                     at<float>(pk, L.mom), at<float>(pk, L.tail), stats);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
+}
+
+int seq_combine_stats_launch(int D, int R, const double* gathered, double* combined, cudaStream_t st) {
+  int Dp = 1;
+  while (Dp < D) Dp <<= 1;
+  k_seq_stats_combine<<<1, 256, 0, st>>>(Dp, R, gathered, combined);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
+}
+
+// Epilogue (+ optional fit step) from global records; identical on every rank.
+int seq_finish_launch(int D, int64_t N_total, int ce, int64_t N_slice, double T,
+                      const double* stats, const double* parts, const float2* fin, float* th,
+                      float* al, float* be, double* lnl, float* gt, float* ga, float* gb,
+                      const FitCfgDev* cfg, void* work, float* opt, float* trace, int32_t* status,
+                      int32_t* iters, int final_eval, const int32_t* pstatus, cudaStream_t st) {
+  const SeqLayout L = make_seq_layout(D, N_slice, ce);
+  SeqWork w = slice_work(D, N_slice, ce, work);
+  const SeqFinishArea a = finish_area(work, L.Dp);
+  k_seq_unpack<<<1, 256, 0, st>>>(D, L.Dp, stats, parts, a.cnt, a.umax, a.mom, a.tail, a.gsum,
+                                  a.gth, a.ls, T);
+  FitCfgDev c0{};
+  const FitCfgDev& c = cfg ? *cfg : c0;
+  const int grad = cfg ? (final_eval ? 0 : 1) : (gt != nullptr);
+  k_seq_finish<<<1, 1024, 0, st>>>(D, L.Dp, T, a.tail, a.cnt, a.umax, a.mom, fin, a.gsum, a.gth,
+                                   a.ls, th, al, be, lnl, gt, ga, gb, grad,
+                                   cfg ? w.ctl : nullptr, c, w.prev, opt ? opt : w.opt, trace,
+                                   N_total, status, iters, pstatus);
+  count_launch(2);
+  return cudaGetLastError() == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
+}
 
 }  // namespace mdhp

@@ -33,7 +33,8 @@ class PackDesc(ctypes.Structure):
 
 class SeqDesc(ctypes.Structure):
     _fields_ = [("D", ctypes.c_int32), ("chunk_events", ctypes.c_int32),
-                ("n_events", ctypes.c_int64), ("T", ctypes.c_double)]
+                ("n_events", ctypes.c_int64), ("T", ctypes.c_double), ("t0", ctypes.c_double),
+                ("has_history", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class FitConfigC(ctypes.Structure):
@@ -104,6 +105,22 @@ def lib() -> ctypes.CDLL:
         L.mdhp_seq_fit.restype = ctypes.c_int
         L.mdhp_seq_fit.argtypes = [ctypes.POINTER(SeqDesc), P, ctypes.POINTER(FitConfigC), P, P, P, P, P,
                                    P, P, P, P]
+        L.mdhp_seq_work_bytes.restype = ctypes.c_size_t
+        L.mdhp_seq_work_bytes.argtypes = [ctypes.POINTER(SeqDesc)]
+        L.mdhp_seq_work_init.restype = ctypes.c_int
+        L.mdhp_seq_work_init.argtypes = [ctypes.POINTER(SeqDesc), P, ctypes.POINTER(FitConfigC), P]
+        L.mdhp_seq_maps.restype = ctypes.c_int
+        L.mdhp_seq_maps.argtypes = [ctypes.POINTER(SeqDesc), P, P, P, P, P, ctypes.c_int32, P]
+        L.mdhp_seq_parts.restype = ctypes.c_int
+        L.mdhp_seq_parts.argtypes = [ctypes.POINTER(SeqDesc), P, P, P, P, P, P, ctypes.c_int32, P, P, P,
+                                     ctypes.c_int32, ctypes.c_int32, P]
+        L.mdhp_seq_stats.restype = ctypes.c_int
+        L.mdhp_seq_stats.argtypes = [ctypes.POINTER(SeqDesc), P, P, P]
+        L.mdhp_seq_stats_combine.restype = ctypes.c_int
+        L.mdhp_seq_stats_combine.argtypes = [ctypes.c_int32, ctypes.c_int32, P, P, P]
+        L.mdhp_seq_finish.restype = ctypes.c_int
+        L.mdhp_seq_finish.argtypes = [ctypes.POINTER(SeqDesc), ctypes.c_int64, P, P, P, P, P, P, P, P, P, P,
+                                      ctypes.POINTER(FitConfigC), P, P, P, P, P, ctypes.c_int32, P, P]
         L.mdhp_packed_layout.restype = ctypes.c_int
         L.mdhp_packed_layout.argtypes = [ctypes.POINTER(PackDesc), P]
         L.mdhp_last_error.restype = ctypes.c_char_p
@@ -298,10 +315,12 @@ class PackedSeq:
         return int(self.desc.D)
 
 
-def seq_pack(D, t, mark, T, chunk_events=256, out: PackedSeq | None = None, stream=None) -> PackedSeq:
-    """mdhp_seq_pack on CUDA tensors t f64[N], mark i32[N] (one sequence on [0, T])."""
+def seq_pack(D, t, mark, T, chunk_events=256, out: PackedSeq | None = None, t0=0.0, has_history=False,
+             stream=None) -> PackedSeq:
+    """mdhp_seq_pack on CUDA tensors t f64[N], mark i32[N] (one sequence on [0, T], or one slice of
+    it starting after t0 when has_history)."""
     _dev(t, torch.float64, "t"); _dev(mark, torch.int32, "mark")
-    desc = SeqDesc(int(D), int(chunk_events), int(t.numel()), float(T))
+    desc = SeqDesc(int(D), int(chunk_events), int(t.numel()), float(T), float(t0), int(bool(has_history)), 0)
     nb = int(lib().mdhp_seq_packed_bytes(ctypes.byref(desc)))
     if nb == 0:
         _check(-2, "mdhp_seq_packed_bytes")

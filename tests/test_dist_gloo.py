@@ -81,3 +81,43 @@ def test_balanced_ranges():
         loads = [c[a:b].sum() for a, b in rr]
         assert max(loads) - min(loads) <= 2 * c.max()
     assert shard.balanced_ranges([5, 0, 0], 4)[-1] == (3, 3) or shard.balanced_ranges([5, 0, 0], 4)[-1][1] == 3
+
+
+def _comm_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2411_10258_b200 import seqdist
+    c = seqdist.TorchComm()
+    g = c.all_gather([torch.full((3, 2), float(rank))])
+    s = c.all_reduce_sum([torch.arange(4, dtype=torch.float64) * (rank + 1)])
+    if rank == 0:
+        ok = g.shape == (world, 3, 2) and all(torch.all(g[r] == r) for r in range(world))
+        ok = ok and torch.equal(s, torch.arange(4, dtype=torch.float64) * sum(r + 1 for r in range(world)))
+        q.put("ok" if ok else "bad")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_seqdist_torchcomm_gloo():
+    """The f1 exchange wrapper (all_gather of maps, all_reduce of partial sums) over gloo."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_comm_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+        assert p.exitcode == 0
+    assert q.get(timeout=5) == "ok"
+
+
+def test_slice_bounds_never_split_ties():
+    from paper_2411_10258_b200 import seqdist
+    t = np.array([0.0, 1.0, 1.0, 1.0, 2.0, 3.0, 3.0, 4.0, 5.0, 6.0])
+    for R in (1, 2, 3, 4, 7, 12):
+        b = seqdist.slice_bounds(t, R)
+        assert b[0][0] == 0 and b[-1][1] == len(t) and all(b[k][1] == b[k + 1][0] for k in range(R - 1))
+        for lo, hi in b:
+            assert lo == 0 or lo == len(t) or t[lo] != t[lo - 1]
