@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-windows", type=int, default=None)
     ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--hidden", type=int, default=128, help="--config feat: MDHP-LSTM hidden size H")
     ap.add_argument("--shard-seq", action="store_true",
                     help="cfg4: split ONE sequence over the ranks (f1, strong scaling, NCCL map exchange)")
     return ap.parse_args()
@@ -55,7 +56,60 @@ WORKLOADS = {
     "cfg3": ("cfg3", 65536),
     "cfg4": ("cfg4", 1),
     "cfg5": ("cfg5", 1 << 20),
+    "feat": ("cfg5", 1 << 20),   # row f4: Hawkes-gate features of cfg5-sized fitted parameters
 }
+
+
+def bench_features(args, world, rank, dev):
+    """--config feat (row f4, not the headline): hks = tanh(A alpha - B (beta T) + C theta)
+    (Eq.(7)) for 1,048,576 windows of D = 16 fitted-like parameters, H = --hidden, on the
+    tcgen05 kernel.  HBM-bound: per window it reads 2D^2+D+1 floats and writes H floats."""
+    import torch
+    import paper_2411_10258_b200 as M
+    D, H = 16, args.hidden
+    W = args.windows or (1 << 20)
+    g = torch.Generator(device=dev).manual_seed(args.seed + rank)
+    al = torch.rand(W, D, D, device=dev, generator=g) * 2
+    be = torch.exp(torch.rand(W, D, D, device=dev, generator=g) * 4.0)
+    th = torch.exp(torch.rand(W, D, device=dev, generator=g) * 6.9 - 3.0)
+    T = torch.ones(W, device=dev)
+    s = (2 * D * D + D) ** -0.5 / 10
+    A = torch.randn(H, D * D, device=dev, generator=g) * s
+    B = torch.randn(H, D * D, device=dev, generator=g) * s
+    C = torch.randn(H, D, device=dev, generator=g) * s
+    out = torch.empty(W, H, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        M.hawkes_features(th, al, be, T, A, B, C, out=out)
+    torch.cuda.synchronize()
+    L0 = M.launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    for k in range(args.steps):
+        ev[2 * k].record(stream)
+        M.hawkes_features(th, al, be, T, A, B, C, out=out)
+        ev[2 * k + 1].record(stream)
+    torch.cuda.synchronize()
+    ms = [ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps)]
+    ms_avg = sum(ms) / len(ms)
+    K = 2 * D * D + D
+    bytes_w = 4 * (K + 1 + H)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    gbs = W * bytes_w / (ms_avg / 1e3) / 1e9
+    tflops = 2.0 * W * K * H / (ms_avg / 1e3) / 1e12
+    if rank == 0:
+        print(json.dumps({
+            "metric": "MDHP-LSTM Hawkes-gate features (Eq.(7) hks) windows/s", "value": W / (ms_avg / 1e3),
+            "unit": "windows/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_avg, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "tf32 (fp32 accumulate)", "data": "synthetic fitted-like parameters, random weights",
+            "config": {"workload": f"feat: {W} windows, D={D}, H={H} (K={K}), inputs {W * 4 * (K + 1) / 1e9:.2f} GB > L2"},
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs / peaks["hbm_gbs"], "traffic": None,
+                         "per_unit": f"{bytes_w} B per window (2D^2+D+1 floats in, H floats out)",
+                         "tensor": {"achieved_tflops": tflops, "peak_tflops_tf32": peaks["bf16_tflops"] / 2,
+                                    "peak_basis": "measured bf16 x 1/2 (nominal tf32:bf16 ratio)"}},
+            "gpu_launches": int(M.launch_count() - L0)}), flush=True)
+    return 0
 
 
 def bench_seq_sharded(args, rc, world, rank, dev):
@@ -315,6 +369,8 @@ def main():
     # ---- synthetic inputs (untimed): windows rank*W .. rank*W+W-1 of the global seeded stream
     if args.config == "cfg4":
         return bench_seq(args, rc, world, rank, dev)
+    if args.config == "feat":
+        return bench_features(args, world, rank, dev)
     first, _ = (rank * W, W)
     b = sgpu.make_batch_gpu(rc, W, seed=args.seed, first_window=first, device=dev)
     E = int(b["win_off"][-1])

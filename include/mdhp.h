@@ -290,6 +290,36 @@ int mdhp_seq_finish(const mdhp_seq_desc* desc, int64_t n_events_total, const dou
  * Dp = D rounded up to a power of two.  Returns MDHP_OK or MDHP_EINVAL / MDHP_EDIM.        */
 int mdhp_packed_layout(const mdhp_pack_desc* desc, size_t offsets[14]);
 
+/* ---------------------------------------------------------------- f4: MDHP-LSTM Hawkes gate */
+/*
+ * mdhp_hawkes_features — SURVEY 8(f) row f4: the Hawkes gate of the MDHP-LSTM cell, Eq.(7)
+ * third line, for every window of a batch of fitted parameters:
+ *
+ *     hks[w][h] = tanh( sum_ij A[h][i*D+j] alpha[w][i][j]
+ *                       - sum_ij B[h][i*D+j] beta[w][i][j] * T_span[w]
+ *                       + sum_j  C[h][j] theta[w][j] )
+ *
+ * (SPEC S:366-381 reading: alpha^x, beta^x flattened row-major, the product beta^x T_span^x
+ * entrywise; computed once per window.)  One tensor-core GEMM (tcgen05 kind::tf32, TMEM
+ * accumulator) with a fused tanh epilogue.  Inputs are rounded to TF32 (round-to-nearest)
+ * before the products, so the pre-activation carries an error <= ~2^-10 * sum_k |W_hk X_wk|
+ * (R22); accumulation is fp32.
+ *
+ *   D                 1..32
+ *   n_windows         W >= 0
+ *   H                 hidden size: a multiple of 16, <= 256, or a multiple of 256
+ *   theta [W][D], alpha [W][D][D], beta [W][D][D]   fp32 device (e.g. mdhp_fit output)
+ *   T_span [W]        fp32 device: window horizon in the parameters' time units
+ *   A [H][D*D], B [H][D*D], C [H][D]                fp32 device, row-major
+ *   hks [W][H]        fp32 device out (16-byte aligned)
+ * Returns MDHP_OK, MDHP_EINVAL (NULL pointer), MDHP_EDIM (D or H out of range), MDHP_ECUDA.
+ * Asynchronous on `stream`; no workspace.
+ */
+int mdhp_hawkes_features(int32_t D, int64_t n_windows, int32_t H, const float* theta,
+                         const float* alpha, const float* beta, const float* T_span,
+                         const float* A, const float* B, const float* C, float* hks,
+                         void* stream);
+
 /* ---------------------------------------------------------------- misc */
 const char* mdhp_last_error(void);   /* thread-local message of the last failing call     */
 uint64_t    mdhp_launch_count(void); /* kernels this library has launched (process-wide)   */

@@ -12,6 +12,7 @@ Functions (see oracle.c for the passages each one follows):
   loglik_rec       same quantity via the eager Ozaki-style recursion, O(N*D^2)
   fit              projected gradient ascent / Adam on lnL
   loglik_batch, fit_batch   pthread pools over CSR windows
+  hawkes_features  MDHP-LSTM Hawkes gate, Eq.(7) third line P:431
 
 Parity status: every function here is pinned by ``tests/test_oracle_pins.py`` (hand values,
 closed forms, brute force, quadrature, finite differences, identities, library Adam).
@@ -105,6 +106,9 @@ def lib():
         L.oracle_fit_batch.restype = None
         L.oracle_fit_batch.argtypes = [ctypes.c_int, ctypes.c_int64, P, P, P, P,
                                        ctypes.POINTER(_FitCfg), P, P, P, P, P, P, ctypes.c_int]
+        L.oracle_hawkes_features.restype = None
+        L.oracle_hawkes_features.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int, P, P, P,
+                                             P, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -215,3 +219,23 @@ def fit_batch(D, t32, mark, win_off, T, theta, alpha, beta, cfg: FitConfig, nthr
     lib().oracle_fit_batch(int(D), W, _p(t32), _p(mark), _p(off), _p(T), ctypes.byref(c),
                            _p(th), _p(al), _p(be), _p(lnl), _p(iters), _p(status), int(nthreads))
     return {"theta": th, "alpha": al, "beta": be, "lnl": lnl, "iters": iters, "status": status}
+
+
+def hawkes_features(D, theta, alpha, beta, T_span, A, B, C, gross=False):
+    """Eq.(7) third line per window: hks[w] = tanh(A alpha_w - B (beta_w T_w) + C theta_w).
+    theta [W][D], alpha/beta [W][D][D], T_span [W], A/B [H][D*D], C [H][D].  -> hks [W][H]
+    (and sum_k |W_hk X_wk| [W][H] when gross=True).  oracle.c: oracle_hawkes_features."""
+    theta = _f64(theta).reshape(-1, D)
+    W = theta.shape[0]
+    alpha = _f64(alpha).reshape(W, D * D)
+    beta = _f64(beta).reshape(W, D * D)
+    T_span = _f64(T_span).reshape(W)
+    A = _f64(A).reshape(-1, D * D)
+    H = A.shape[0]
+    B = _f64(B).reshape(H, D * D)
+    C = _f64(C).reshape(H, D)
+    out = np.empty((W, H))
+    g = np.empty((W, H)) if gross else None
+    lib().oracle_hawkes_features(int(D), W, H, _p(theta), _p(alpha), _p(beta), _p(T_span), _p(A),
+                                 _p(B), _p(C), _p(out), _p(g))
+    return (out, g) if gross else out

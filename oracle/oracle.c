@@ -22,6 +22,9 @@
  *   oracle_fit             projected gradient ascent on lnL with the
  *                          optimizer/stopping definition of DESIGN.md section "Fit".
  *   *_batch                the same over many windows, on a pthread pool.
+ *   oracle_hawkes_features the MDHP-LSTM Hawkes gate, Eq.(7) third line:
+ *                          hks = tanh(A alpha - B (beta T_span) + C theta) per window
+ *                          (SURVEY 8(f) row f4), plain loops in fp64.
  *
  * Conventions: alpha, beta are D*D row-major [i][j] = target i, source j (Eq.(2) P:107:
  * lambda^i sums over sources j).  theta is length D.  Times are fp64: the fp32 analysis times
@@ -480,4 +483,38 @@ void oracle_fit_batch(int D, int64_t W, const double* t, const int32_t* mark,
     J.theta = theta; J.alpha = alpha; J.beta = beta; J.lnl = lnl;
     J.cfg = cfg; J.iters = iters; J.status = status;
     run_batch(&J, nthreads);
+}
+
+/* ---- Eq.(7) third line: hks^t = tanh(A alpha^x - B (beta^x T_span^x) + C theta^x).
+ * alpha^x, beta^x are the window's D*D matrices flattened row-major (index i*D+j), the product
+ * beta^x T_span^x entrywise (SPEC S:366-374 reading), theta^x the D baselines.  A, B are
+ * H x D*D and C is H x D, row-major.  hks is W x H.  gross (optional, W x H) receives
+ * sum_k |W_hk X_wk| of the pre-activation, the scale of its rounding error on other hardware. */
+void oracle_hawkes_features(int D, int64_t W, int H, const double* theta, const double* alpha,
+                            const double* beta, const double* T_span, const double* A,
+                            const double* B, const double* C, double* hks, double* gross)
+{
+    const int DD = D * D;
+    for (int64_t w = 0; w < W; w++) {
+        const double* al = alpha + w * DD;
+        const double* be = beta + w * DD;
+        const double* th = theta + w * D;
+        for (int h = 0; h < H; h++) {
+            double z = 0.0, g = 0.0;
+            for (int k = 0; k < DD; k++) {
+                z += A[(int64_t)h * DD + k] * al[k];
+                g += fabs(A[(int64_t)h * DD + k] * al[k]);
+            }
+            for (int k = 0; k < DD; k++) {
+                z -= B[(int64_t)h * DD + k] * (be[k] * T_span[w]);
+                g += fabs(B[(int64_t)h * DD + k] * (be[k] * T_span[w]));
+            }
+            for (int j = 0; j < D; j++) {
+                z += C[(int64_t)h * D + j] * th[j];
+                g += fabs(C[(int64_t)h * D + j] * th[j]);
+            }
+            hks[w * H + h] = tanh(z);
+            if (gross) gross[w * H + h] = g;
+        }
+    }
 }

@@ -18,6 +18,9 @@ int fit_launch(const Packed& P, const FitCfgDev& cfg, float* th, float* al, floa
                double* lnl, int32_t* iters, int32_t* status, float* trace, int* counter,
                cudaStream_t st);
 
+int features_launch(int D, int64_t W, int H, const float* theta, const float* alpha,
+                    const float* beta, const float* T, const float* A, const float* B,
+                    const float* C, float* hks, cudaStream_t st);
 int dense_launch(const Packed& P, const float* th, const float* al, const float* be, double* lnl,
                  const int32_t* status, cudaStream_t st);
 int seq_pack_launch(int D, int64_t N, int ce, double T, double t0, const double* t,
@@ -229,6 +232,33 @@ int mdhp_loglik_dense(const mdhp_pack_desc* d, const void* packed, const float* 
   rc = dense_launch(view(L, packed), theta, alpha, beta, loglik, win_status, (cudaStream_t)stream);
   if (rc) return rc;
   return check_cuda("mdhp_loglik_dense");
+}
+
+int mdhp_hawkes_features(int32_t D, int64_t W, int32_t H, const float* theta,
+                         const float* alpha, const float* beta, const float* T_span,
+                         const float* A, const float* B, const float* C, float* hks,
+                         void* stream) {
+  if (D < 1 || D > 32 || W < 0) {
+    set_error("D=%d outside 1..32 or W=%lld < 0", D, (long long)W);
+    return MDHP_EDIM;
+  }
+  if (H < 16 || H % 16 != 0 || (H > 256 && H % 256 != 0)) {
+    set_error("H=%d: need a multiple of 16 up to 256, or a multiple of 256", H);
+    return MDHP_EDIM;
+  }
+  if (W == 0) return MDHP_OK;   // nothing to read or write (empty tensors may carry NULL)
+  if (!theta || !alpha || !beta || !T_span || !A || !B || !C || !hks) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  if (reinterpret_cast<uintptr_t>(hks) % 16 != 0) {
+    set_error("hks must be 16-byte aligned");
+    return MDHP_EINVAL;
+  }
+  const int rc = features_launch(D, W, H, theta, alpha, beta, T_span, A, B, C, hks,
+                                 (cudaStream_t)stream);
+  if (rc) return rc;
+  return check_cuda("mdhp_hawkes_features");
 }
 
 int mdhp_fit(const mdhp_pack_desc* d, const void* packed, const mdhp_fit_config* cfg, float* theta,

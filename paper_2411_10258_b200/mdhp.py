@@ -90,6 +90,9 @@ def lib() -> ctypes.CDLL:
         L.mdhp_loglik_grad.argtypes = [ctypes.POINTER(PackDesc), P, P, P, P, P, P, P, P, P, P]
         L.mdhp_loglik_dense.restype = ctypes.c_int
         L.mdhp_loglik_dense.argtypes = [ctypes.POINTER(PackDesc), P, P, P, P, P, P, P]
+        L.mdhp_hawkes_features.restype = ctypes.c_int
+        L.mdhp_hawkes_features.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, P, P, P, P,
+                                           P, P, P, P, P]
         L.mdhp_fit.restype = ctypes.c_int
         L.mdhp_fit.argtypes = [ctypes.POINTER(PackDesc), P, ctypes.POINTER(FitConfigC), P, P, P, P, P,
                                P, P, P, P]
@@ -259,6 +262,22 @@ def loglik_dense(pk: Packed, theta, alpha, beta, out=None, stream=None):
                                  _ptr(lnl), _ptr(pk.status), _stream(stream))
     _check(rc, "mdhp_loglik_dense")
     return lnl
+
+
+def hawkes_features(theta, alpha, beta, T_span, A, B, C, out=None, stream=None):
+    """mdhp_hawkes_features (row f4): hks[w] = tanh(A alpha_w - B (beta_w T_w) + C theta_w),
+    Eq.(7) third line.  theta [W][D], alpha/beta [W][D][D], T_span [W], A/B [H][D*D],
+    C [H][D], all fp32 CUDA tensors.  -> hks fp32 [W][H]."""
+    for nm, x in (("theta", theta), ("alpha", alpha), ("beta", beta), ("T_span", T_span),
+                  ("A", A), ("B", B), ("C", C)):
+        _dev(x, torch.float32, nm)
+    W, D = theta.shape[0], theta.shape[-1]
+    H = A.shape[0]
+    hks = out if out is not None else torch.empty(W, H, dtype=torch.float32, device=theta.device)
+    rc = lib().mdhp_hawkes_features(D, W, H, _ptr(theta), _ptr(alpha), _ptr(beta), _ptr(T_span),
+                                    _ptr(A), _ptr(B), _ptr(C), _ptr(hks), _stream(stream))
+    _check(rc, "mdhp_hawkes_features")
+    return hks
 
 
 def fit(pk: Packed, theta, alpha, beta, cfg: FitConfig, opt_state=None, trace=False, stream=None):

@@ -82,3 +82,16 @@ def test_no_cpu_fallback():
     with pytest.raises(TypeError):
         M.pack_windows(2, torch.zeros(3, dtype=torch.float64), torch.zeros(3, dtype=torch.int32),
                        torch.tensor([0, 3]), torch.ones(1, dtype=torch.float64))
+
+
+def test_hawkes_features_args_rejected_without_gpu():
+    L = M.lib()
+    fake = ctypes.c_void_p(16)
+    args = [fake] * 7 + [ctypes.c_void_p(256), None]
+    assert L.mdhp_hawkes_features(0, 4, 16, *args) == -2          # D out of range
+    assert L.mdhp_hawkes_features(33, 4, 16, *args) == -2
+    assert L.mdhp_hawkes_features(4, 4, 24, *args) == -2          # H not a multiple of 16
+    assert L.mdhp_hawkes_features(4, 4, 272, *args) == -2         # H > 256 not a multiple of 256
+    assert L.mdhp_hawkes_features(4, 4, 16, None, *args[1:]) == -1
+    assert b"NULL" in L.mdhp_last_error()
+    assert L.mdhp_hawkes_features(4, 4, 16, *args[:7], ctypes.c_void_p(260), None) == -1   # unaligned out
