@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-windows", type=int, default=None)
     ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--inject", default="none", choices=["none", "PLA", "DEA", "ASA", "DAM"],
+                    help="time-exciting injections (Table II + Algorithm 4) in attack windows (row f2)")
     ap.add_argument("--hidden", type=int, default=128, help="--config feat: MDHP-LSTM hidden size H")
     ap.add_argument("--shard-seq", action="store_true",
                     help="cfg4: split ONE sequence over the ranks (f1, strong scaling, NCCL map exchange)")
@@ -95,6 +97,12 @@ def bench_features(args, world, rank, dev):
     bytes_w = 4 * (K + 1 + H)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     gbs = W * bytes_w / (ms_avg / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "r01_features_traffic.json")
+    if os.path.exists(tf):
+        tj = json.load(open(tf))
+        if tj["config"]["D"] == D and tj["config"]["H"] == H:
+            traffic = tj["per_window_bytes"] * W   # DRAM bytes per launch (ncu capture, scaled by W)
     tflops = 2.0 * W * K * H / (ms_avg / 1e3) / 1e12
     if rank == 0:
         print(json.dumps({
@@ -104,8 +112,9 @@ def bench_features(args, world, rank, dev):
             "dtype": "tf32 (fp32 accumulate)", "data": "synthetic fitted-like parameters, random weights",
             "config": {"workload": f"feat: {W} windows, D={D}, H={H} (K={K}), inputs {W * 4 * (K + 1) / 1e9:.2f} GB > L2"},
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": gbs / peaks["hbm_gbs"], "traffic": None,
+                         "frac": gbs / peaks["hbm_gbs"], "traffic": traffic,
                          "per_unit": f"{bytes_w} B per window (2D^2+D+1 floats in, H floats out)",
+                         "kernel": "k_hawkes_features_tma",
                          "tensor": {"achieved_tflops": tflops, "peak_tflops_tf32": peaks["bf16_tflops"] / 2,
                                     "peak_basis": "measured bf16 x 1/2 (nominal tf32:bf16 ratio)"}},
             "gpu_launches": int(M.launch_count() - L0)}), flush=True)
@@ -305,6 +314,9 @@ def reference_arm(args):
     from synth import gen
     rname, _ = WORKLOADS[args.config]
     rc = gen.CONFIGS[rname]
+    if args.inject != "none":
+        import dataclasses
+        rc = dataclasses.replace(rc, inject=args.inject)
     D = rc.D
     nw = args.cpu_windows or 512
     it = 5
@@ -362,6 +374,9 @@ def main():
 
     rname, wdef = WORKLOADS[args.config]
     rc = gen.CONFIGS[rname]
+    if args.inject != "none":
+        import dataclasses
+        rc = dataclasses.replace(rc, inject=args.inject)
     D = rc.D
     W = args.windows or wdef
     stream = torch.cuda.current_stream()
@@ -498,7 +513,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": f"synthetic (Ogata-thinned MDHP on GPU, recipe {rname}, seed {args.seed})",
+            "data": f"synthetic (Ogata-thinned MDHP on GPU, recipe {rname}, seed {args.seed}"
+                    + (f", {args.inject} injections in attack windows" if args.inject != "none" else "") + ")",
             "config": {"workload": f"{args.config}: {W} windows/GPU, D={D}, ~{E // max(W, 1)} events/window, "
                                    f"T={rc.T}s, Adam lr 0.05, {args.iters} fixed iterations + final eval",
                        "windows_per_gpu": W, "events_per_gpu": E, "D": D, "iterations": args.iters,

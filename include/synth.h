@@ -51,6 +51,30 @@ int synth_ogata(int32_t D, int64_t W, int64_t first_window, uint64_t seed, doubl
                 const int64_t* win_off, int64_t* counts, double* t_out, int32_t* mark_out,
                 void* stream);
 
+/* Time-exciting injection strategies (Table II): attack-rate shapes g(u) on the
+ * normalised window u = t/T in [0,1]; constants in DESIGN.md R23.                   */
+#define SYNTH_NONE 0
+#define SYNTH_PLA  1   /* power-law acceleration   g = a u^b                                  */
+#define SYNTH_DEA  2   /* delayed escalation       W1 a1 u^(a1-1) | W2 a2 e^{gamma (u - t1)}   */
+#define SYNTH_ASA  3   /* adaptive stealth         C e^{gamma u} / (1 + e^{gamma (u - t0)})^2  */
+#define SYNTH_DAM  4   /* multi-strategy           w a1 u^(a1-1) + (1 - w) a2 e^{a2 u}         */
+
+/* synth_ogata plus injections: in every window with attack[w] != 0, an independent
+ * Algorithm-4 (NPP) stream — candidate gaps Exponential(mean 1/inj_rate) in u,
+ * accepted with probability g(u)/g_max — is superposed on the Hawkes events, all on one ID
+ * drawn uniformly per window; the Hawkes part is the same stream synth_ogata produces.
+ * strategy SYNTH_NONE ignores attack (then it equals synth_ogata).                          */
+int synth_ogata_inject(int32_t D, int64_t W, int64_t first_window, uint64_t seed, double T,
+                       const float* theta, const float* alpha, const float* beta,
+                       int64_t max_events, const int64_t* win_off, int64_t* counts,
+                       double* t_out, int32_t* mark_out, const uint8_t* attack,
+                       int32_t strategy, double inj_rate, void* stream);
+
+/* The injection sampler alone (Algorithm 4 on [0,1], same stream as synth_ogata_inject):
+ * count pass (win_off == NULL) -> counts[w]; write pass -> normalised times u_out.        */
+int synth_npp(int64_t W, int64_t first_window, uint64_t seed, int32_t strategy, double rate,
+              const int64_t* win_off, int64_t* counts, double* u_out, void* stream);
+
 const char* synth_last_error(void);
 
 #ifdef __cplusplus

@@ -122,6 +122,44 @@ __global__ void k_params(int D, int64_t W, int64_t first, uint64_t seed, synth_r
   if (attack) attack[w] = att ? 1 : 0;
 }
 
+// ---- Time-exciting injection: the four attack-rate shapes of Table II
+// on the normalised window u = t / T in [0, 1], sampled by Algorithm 4
+// (NPP): candidate gaps Exponential with mean 1/512 (S:337 reading), accept with
+// probability g(u)/g_max.  Constants: DESIGN.md R23.
+__host__ __device__ inline double attack_rate(int strat, double u) {
+  switch (strat) {
+    case SYNTH_PLA: return 1.0 * u * u;                                     // a t^b, a=1, b=2
+    case SYNTH_DEA: return u < 0.6 ? 1.0 * 2.0 * u                          // W1 a1 t^(a1-1)
+                                   : 1.0 * 1.2 * exp(4.0 * (u - 0.6));      // W2 a2 e^{g(t-t1)}
+    case SYNTH_ASA: {
+      const double e = exp(10.0 * (u - 0.5));
+      return exp(10.0 * u) / ((1.0 + e) * (1.0 + e));                       // C e^{gt}/(1+e^{g(t-t0)})^2
+    }
+    case SYNTH_DAM: return 0.5 * 3.0 * u * u + 0.5 * 4.0 * exp(4.0 * u);     // w a1 t^(a1-1) + (1-w) a2 e^{a2 t}
+    default: return 0.0;
+  }
+}
+
+// max of g on [0, 1] by dense evaluation (Algorithm 6's "max(evaluate g(t))").
+__host__ __device__ inline double attack_rate_max(int strat) {
+  double m = 0.0;
+  for (int k = 0; k <= 4096; k++) m = fmax(m, attack_rate(strat, k / 4096.0));
+  return m * (1.0 + 1e-9);
+}
+
+// Algorithm 4 as a generator: next accepted normalised time (> 1 when exhausted).
+struct Npp {
+  int strat;
+  double gmax, u, rate;
+  __device__ double next(Rng& R) {
+    while (true) {
+      u += -log(R.uniform()) / rate;      // Delta t ~ Exponential(mean 1/rate)
+      if (u > 1.0) return 2.0;
+      if (R.uniform() * gmax < attack_rate(strat, u)) return u;
+    }
+  }
+};
+
 constexpr int kWPB = 4;
 
 template <int RP>
@@ -129,7 +167,8 @@ __global__ void __launch_bounds__(kWPB * 32)
 k_ogata(int D, int64_t W, int64_t first, uint64_t seed, double T, const float* __restrict__ theta,
         const float* __restrict__ alpha, const float* __restrict__ beta, int64_t max_events,
         const int64_t* __restrict__ win_off, int64_t* __restrict__ counts,
-        double* __restrict__ t_out, int32_t* __restrict__ mark_out) {
+        double* __restrict__ t_out, int32_t* __restrict__ mark_out,
+        const uint8_t* __restrict__ attack, int strat, double inj_rate) {
   __shared__ float v[kWPB][RP * 32];
   const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t w = (int64_t)blockIdx.x * kWPB + wp;
@@ -152,6 +191,14 @@ k_ogata(int D, int64_t W, int64_t first, uint64_t seed, double T, const float* _
   int64_t n = 0;
   const int64_t base = win_off ? win_off[w] : 0;
   bool overflow = false;
+  // injections (attack windows only): an independent stream superposed on the Hawkes traffic,
+  // all on one randomly chosen ID ("one IP is randomly selected"); every lane runs the
+  // same generator so the warp stays uniform
+  const bool inject = strat != SYNTH_NONE && attack && attack[w];
+  Rng RI(seed, (uint64_t)(first + w), 3u);
+  Npp npp{strat, inject ? attack_rate_max(strat) : 1.0, 0.0, inj_rate};
+  const int inj_dim = inject ? min((int)(RI.uniform() * D), D - 1) : 0;
+  double inj_t = inject ? npp.next(RI) * T : 3.0 * T;
   while (bound > 0.0f) {
     const double u1 = R.uniform();
     const double u2 = R.uniform();
@@ -181,6 +228,14 @@ k_ogata(int D, int64_t W, int64_t first, uint64_t seed, double T, const float* _
     if (u <= total) {
       const unsigned bal = __ballot_sync(0xffffffffu, lane < D && cum >= u);
       const int i = bal ? (__ffs(bal) - 1) : D - 1;
+      while (inj_t <= now) {
+        if (win_off && lane == 0) {
+          t_out[base + n] = inj_t;
+          mark_out[base + n] = inj_dim;
+        }
+        n++;
+        inj_t = npp.next(RI) * T;
+      }
       if (win_off && lane == 0) {
         t_out[base + n] = now;
         mark_out[base + n] = i;
@@ -203,6 +258,15 @@ k_ogata(int D, int64_t W, int64_t first, uint64_t seed, double T, const float* _
     for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     bound = sth + s;
   }
+  while (!overflow && inj_t <= T) {
+    if (win_off && lane == 0) {
+      t_out[base + n] = inj_t;
+      mark_out[base + n] = inj_dim;
+    }
+    n++;
+    if (n > max_events) overflow = true;
+    inj_t = npp.next(RI) * T;
+  }
   if (!win_off && lane == 0) counts[w] = overflow ? -1 : n;
 }
 
@@ -211,6 +275,42 @@ k_ogata(int D, int64_t W, int64_t first, uint64_t seed, double T, const float* _
 extern "C" {
 
 const char* synth_last_error(void) { return g_err; }
+
+namespace {
+__global__ void k_npp(int64_t W, int64_t first, uint64_t seed, int strat, double rate,
+                      const int64_t* __restrict__ off, int64_t* __restrict__ counts,
+                      double* __restrict__ u_out) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= W) return;
+  Rng R(seed, (uint64_t)(first + w), 3u);
+  Npp npp{strat, attack_rate_max(strat), 0.0, rate};
+  (void)R.uniform();   // the injected-ID draw of k_ogata (same stream layout)
+  int64_t n = 0;
+  for (double u = npp.next(R); u <= 1.0; u = npp.next(R)) {
+    if (off) u_out[off[w] + n] = u;
+    n++;
+  }
+  if (!off) counts[w] = n;
+}
+}  // namespace
+
+int synth_npp(int64_t W, int64_t first_window, uint64_t seed, int32_t strategy, double rate,
+              const int64_t* win_off, int64_t* counts, double* u_out, void* stream) {
+  if (W < 0 || strategy <= SYNTH_NONE || strategy > SYNTH_DAM || !(rate > 0.0) ||
+      (!win_off && !counts) || (win_off && !u_out)) {
+    err("synth_npp: bad arguments");
+    return -1;
+  }
+  if (W == 0) return 0;
+  k_npp<<<(unsigned)((W + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      W, first_window, seed, strategy, rate, win_off, counts, u_out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err("synth_npp: %s", cudaGetErrorString(e));
+    return -5;
+  }
+  return 0;
+}
 
 int synth_params(int32_t D, int64_t W, int64_t first_window, uint64_t seed, const synth_recipe* rc,
                  float* theta, float* alpha, float* beta, uint8_t* attack, void* stream) {
@@ -234,6 +334,20 @@ int synth_ogata(int32_t D, int64_t W, int64_t first_window, uint64_t seed, doubl
                 const float* theta, const float* alpha, const float* beta, int64_t max_events,
                 const int64_t* win_off, int64_t* counts, double* t_out, int32_t* mark_out,
                 void* stream) {
+  return synth_ogata_inject(D, W, first_window, seed, T, theta, alpha, beta, max_events, win_off,
+                            counts, t_out, mark_out, nullptr, SYNTH_NONE, 512.0, stream);
+}
+
+int synth_ogata_inject(int32_t D, int64_t W, int64_t first_window, uint64_t seed, double T,
+                       const float* theta, const float* alpha, const float* beta,
+                       int64_t max_events, const int64_t* win_off, int64_t* counts,
+                       double* t_out, int32_t* mark_out, const uint8_t* attack,
+                       int32_t strategy, double inj_rate, void* stream) {
+  if (strategy < SYNTH_NONE || strategy > SYNTH_DAM || (strategy != SYNTH_NONE && !attack) ||
+      !(inj_rate > 0.0)) {
+    err("synth_ogata_inject: bad strategy/attack/rate");
+    return -1;
+  }
   if (D < 1 || D > 32 || W < 0 || !theta || !alpha || !beta || !(T > 0.0) ||
       (!win_off && !counts) || (win_off && (!t_out || !mark_out))) {
     err("synth_ogata: bad arguments");
@@ -245,7 +359,8 @@ int synth_ogata(int32_t D, int64_t W, int64_t first_window, uint64_t seed, doubl
   const int rp = (D * D + 31) / 32;
 #define SYNTH_LAUNCH(RPV) \
   k_ogata<RPV><<<blocks, kWPB * 32, 0, st>>>(D, W, first_window, seed, T, theta, alpha, beta, \
-                                             max_events, win_off, counts, t_out, mark_out)
+                                             max_events, win_off, counts, t_out, mark_out, \
+                                             attack, strategy, inj_rate)
   if (rp <= 1) SYNTH_LAUNCH(1);
   else if (rp <= 2) SYNTH_LAUNCH(2);
   else if (rp <= 4) SYNTH_LAUNCH(4);

@@ -12,6 +12,8 @@ likelihood / gradient / fit arithmetic; it only *simulates* event streams:
                      self + k cross excitations, attack bursts on n_a IDs; 50% attack
                      windows as in STEIA9, P:526).
 * ``make_batch``     CSR batch (t fp64[E], mark i32[E], win_off i64[W+1], T f64[W]).
+* ``attack_rate``, ``npp_sample``  the Table II attack-rate shapes and Algorithm 4
+                     (NPP thinning) for time-exciting injections (row f2).
 * ``edge_windows``   hand-built edge cases (empty window, empty dims, cross-dim ties,
                      events at t = 0 and t = T, a single event).
 
@@ -81,6 +83,8 @@ class Recipe:
     attack_frac: float = 0.5
     n_attack: int = 1
     rho_attack: float = 0.9
+    inject: str = "none"        # injection strategy in attack windows: none | PLA | DEA | ASA | DAM
+    inj_rate: float = 512.0     # Algorithm 4 candidate rate per unit normalised time
 
 
 CONFIGS = {
@@ -98,6 +102,43 @@ CFG1_PARAMS = dict(  # BASELINE cfg1 / SURVEY 8(d): rho = 0.612, stationary E[N]
     alpha=np.array([[0.8, 0.4], [0.3, 0.9]]),
     beta=np.array([[2.0, 1.5], [1.5, 2.5]]),
 )
+
+
+STRATEGIES = {"none": 0, "PLA": 1, "DEA": 2, "ASA": 3, "DAM": 4}
+
+
+def attack_rate(strategy: str, u):
+    """Table II attack-rate shapes on the normalised window u in [0, 1] with
+    the constants of DESIGN.md R23."""
+    u = np.asarray(u, dtype=np.float64)
+    if strategy == "PLA":                      # a t^b
+        return 1.0 * u ** 2
+    if strategy == "DEA":                      # W1 a1 t^(a1-1) | W2 a2 e^{gamma (t - t1)}
+        return np.where(u < 0.6, 1.0 * 2.0 * u, 1.0 * 1.2 * np.exp(4.0 * (u - 0.6)))
+    if strategy == "ASA":                      # C e^{gamma t} / (1 + e^{gamma (t - t0)})^2
+        return np.exp(10.0 * u) / (1.0 + np.exp(10.0 * (u - 0.5))) ** 2
+    if strategy == "DAM":                      # w a1 t^(a1-1) + (1 - w) a2 e^{a2 t}
+        return 0.5 * 3.0 * u ** 2 + 0.5 * 4.0 * np.exp(4.0 * u)
+    raise ValueError(strategy)
+
+
+def attack_rate_max(strategy: str) -> float:
+    """max of g on [0, 1] by dense evaluation (Algorithm 6's "max(evaluate g(t))")."""
+    return float(attack_rate(strategy, np.arange(4097) / 4096.0).max()) * (1.0 + 1e-9)
+
+
+def npp_sample(strategy: str, rng: np.random.Generator, rate: float = 512.0, t_min=0.0, t_max=1.0):
+    """Algorithm 4: candidate gaps Exponential(mean 1/rate), accept a candidate t
+    with u ~ Uniform(0, g_max) < g(t).  Returns the accepted times (ascending)."""
+    gmax = attack_rate_max(strategy)
+    t, out = t_min, []
+    while t < t_max:
+        t += rng.exponential(1.0 / rate)
+        if t > t_max:
+            break
+        if rng.uniform(0.0, gmax) < float(attack_rate(strategy, t)):
+            out.append(t)
+    return np.asarray(out, dtype=np.float64)
 
 
 def recipe_params(rc: Recipe, rng: np.random.Generator):
@@ -148,6 +189,12 @@ def make_batch(rc: Recipe, W: int, seed: int = 2024, first_window: int = 0, para
             th, al, be = (np.asarray(params[k], dtype=np.float64) for k in ("theta", "alpha", "beta"))
             a = False
         t, m = ogata_window(th, al, be, rc.T, rng)
+        if a and rc.inject != "none":
+            # injections superposed on the Hawkes traffic, on one random ID
+            k = int(rng.integers(D))
+            ti = npp_sample(rc.inject, rng, rc.inj_rate) * rc.T
+            t = np.concatenate([t, ti]); m = np.concatenate([m, np.full(len(ti), k, np.int32)])
+            o = np.argsort(t, kind="stable"); t, m = t[o], m[o]
         ts.append(t); ms.append(m); offs.append(offs[-1] + len(t))
         TH[w], AL[w], BE[w], att[w] = th, al, be, a
     return {

@@ -8,7 +8,7 @@ import subprocess
 
 import torch
 
-from .gen import CONFIGS, Recipe
+from .gen import CONFIGS, STRATEGIES, Recipe
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -47,6 +47,13 @@ def lib():
         L.synth_ogata.restype = ctypes.c_int
         L.synth_ogata.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64,
                                   ctypes.c_double, P, P, P, ctypes.c_int64, P, P, P, P, P]
+        L.synth_ogata_inject.restype = ctypes.c_int
+        L.synth_ogata_inject.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64,
+                                         ctypes.c_double, P, P, P, ctypes.c_int64, P, P, P, P, P,
+                                         ctypes.c_int32, ctypes.c_double, P]
+        L.synth_npp.restype = ctypes.c_int
+        L.synth_npp.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double,
+                                P, P, P, P]
         L.synth_last_error.restype = ctypes.c_char_p
         _lib = L
     return _lib
@@ -85,10 +92,13 @@ def make_batch_gpu(rc: Recipe | str, W: int, seed: int = 2024, first_window: int
     else:
         th, al, be = (params[k].to(device=device, dtype=torch.float32).contiguous() for k in ("theta", "alpha", "beta"))
         att = torch.zeros(W, dtype=torch.uint8, device=device)
-    cap = int(max_events or max(64, 16 * rc.total_rate * rc.T))
+    cap = int(max_events or max(64, 16 * rc.total_rate * rc.T + 2 * rc.inj_rate))
     counts = torch.empty(W, dtype=torch.int64, device=device)
-    _check(lib().synth_ogata(D, W, first_window, seed, rc.T, _p(th), _p(al), _p(be), cap, None, _p(counts),
-                             None, None, st), "synth_ogata(count)")
+    strat = STRATEGIES[rc.inject]
+    att_p = _p(att) if strat else None
+    _check(lib().synth_ogata_inject(D, W, first_window, seed, rc.T, _p(th), _p(al), _p(be), cap, None,
+                                    _p(counts), None, None, att_p, strat, rc.inj_rate, st),
+           "synth_ogata(count)")
     if bool((counts < 0).any()):
         raise RuntimeError("synth_ogata: a window exceeded max_events")
     off = torch.zeros(W + 1, dtype=torch.int64, device=device)
@@ -96,8 +106,23 @@ def make_batch_gpu(rc: Recipe | str, W: int, seed: int = 2024, first_window: int
     E = int(off[-1])
     t = torch.empty(max(E, 1), dtype=torch.float64, device=device)[:E]
     m = torch.empty(max(E, 1), dtype=torch.int32, device=device)[:E]
-    _check(lib().synth_ogata(D, W, first_window, seed, rc.T, _p(th), _p(al), _p(be), cap, _p(off), _p(counts),
-                             _p(t), _p(m), st), "synth_ogata(write)")
+    _check(lib().synth_ogata_inject(D, W, first_window, seed, rc.T, _p(th), _p(al), _p(be), cap, _p(off),
+                                    _p(counts), _p(t), _p(m), att_p, strat, rc.inj_rate, st),
+           "synth_ogata(write)")
     T = torch.full((W,), rc.T, dtype=torch.float64, device=device)
     return {"D": D, "t": t, "mark": m, "win_off": off, "T": T, "theta": th, "alpha": al, "beta": be,
             "attack": att}
+
+
+def npp_gpu(strategy: str, W: int, seed: int = 2024, first_window: int = 0, rate: float = 512.0, device="cuda"):
+    """Algorithm 4 injection times alone (normalised u in [0, 1]) for W windows -> (u f64[E], off i64[W+1]),
+    the same streams synth_ogata_inject superposes on attack windows."""
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    counts = torch.empty(W, dtype=torch.int64, device=device)
+    k = STRATEGIES[strategy]
+    _check(lib().synth_npp(W, first_window, seed, k, rate, None, _p(counts), None, st), "synth_npp(count)")
+    off = torch.zeros(W + 1, dtype=torch.int64, device=device)
+    torch.cumsum(counts, 0, out=off[1:])
+    u = torch.empty(max(int(off[-1]), 1), dtype=torch.float64, device=device)
+    _check(lib().synth_npp(W, first_window, seed, k, rate, _p(off), _p(counts), _p(u), st), "synth_npp(write)")
+    return u[:int(off[-1])], off

@@ -98,3 +98,98 @@ def test_gpu_generator_statistics():
     b2 = sg.make_batch_gpu("cfg5", 4, seed=2024, first_window=12)
     s = int(b1["win_off"][12])
     assert torch.equal(b1["t"][s:], b2["t"]) and torch.equal(b1["alpha"][12:], b2["alpha"])
+
+
+# ---- row f2: time-exciting injections (Table II shapes, Algorithm 4 NPP) ----
+from scipy import integrate  # noqa: E402
+
+STRATS = ["PLA", "DEA", "ASA", "DAM"]
+
+
+def _bin_expect(strategy, rate, edges):
+    """Expected accepted count per bin: rate * int_bin g / g_max (Algorithm 4 thins a Poisson
+    candidate stream of the given rate with acceptance g/g_max)."""
+    gmax = gen.attack_rate_max(strategy)
+    f = lambda u: float(gen.attack_rate(strategy, u)) / gmax
+    return np.array([rate * integrate.quad(f, a, b, points=[0.6])[0] for a, b in zip(edges[:-1], edges[1:])])
+
+
+def _chi2_ok(counts, expect):
+    chi = ((counts - expect) ** 2 / expect).sum()
+    return stats.chi2.sf(chi, len(counts) - 1) > 1e-3
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_npp_sampler_integral_proportional(strategy):
+    """SPEC's sampler property: quartile-bin counts proportional to int g (chi-square), and the
+    total count Poisson with mean rate * int g / g_max (Algorithm 4)."""
+    rng = np.random.default_rng(42)
+    edges = np.linspace(0, 1, 5)
+    runs = [gen.npp_sample(strategy, rng, rate=512.0) for _ in range(200)]
+    allu = np.concatenate(runs)
+    assert all(np.all(np.diff(r) > 0) for r in runs)
+    assert allu.min() > 0 and allu.max() <= 1.0
+    counts = np.histogram(allu, edges)[0]
+    exp = _bin_expect(strategy, 512.0 * len(runs), edges)
+    assert _chi2_ok(counts, exp), (counts, exp)
+
+
+def test_injection_superposed_on_attack_windows_only():
+    rc = gen.Recipe(D=4, T=2.0, total_rate=40.0, attack_frac=0.5, inject="PLA", inj_rate=256.0)
+    rc0 = gen.Recipe(D=4, T=2.0, total_rate=40.0, attack_frac=0.5)
+    a = gen.make_batch(rc, 30, seed=3)
+    b = gen.make_batch(rc0, 30, seed=3)
+    for w in range(30):
+        na = a["win_off"][w + 1] - a["win_off"][w]
+        nb = b["win_off"][w + 1] - b["win_off"][w]
+        if a["attack"][w]:
+            assert na >= nb
+        else:
+            assert na == nb
+        t = a["t"][a["win_off"][w]:a["win_off"][w + 1]]
+        assert np.all(np.diff(t) >= 0) and (len(t) == 0 or t.max() <= rc.T)
+    assert sum(a["win_off"][1:] - a["win_off"][:-1]) > sum(b["win_off"][1:] - b["win_off"][:-1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("strategy", STRATS)
+def test_gpu_npp_sampler_integral_proportional(strategy):
+    from synth import gpu as sg
+    W = 400
+    u, off = sg.npp_gpu(strategy, W, seed=9, rate=512.0)
+    u = u.cpu().numpy(); off = off.cpu().numpy()
+    assert u.min() > 0 and u.max() <= 1.0
+    assert all(np.all(np.diff(u[off[w]:off[w + 1]]) > 0) for w in range(W))
+    edges = np.linspace(0, 1, 5)
+    counts = np.histogram(u, edges)[0]
+    assert _chi2_ok(counts, _bin_expect(strategy, 512.0 * W, edges)), counts
+
+
+@pytest.mark.gpu
+def test_gpu_injection_is_exact_superposition():
+    """synth_ogata_inject = the Hawkes stream of synth_ogata merged with the NPP stream on one ID,
+    in attack windows only (the same Philox streams)."""
+    import dataclasses
+    from synth import gpu as sg
+    rc0 = gen.CONFIGS["cfg2"]
+    rc = dataclasses.replace(rc0, inject="DAM")
+    W = 64
+    a = sg.make_batch_gpu(rc, W, seed=12)
+    b = sg.make_batch_gpu(rc0, W, seed=12)
+    u, uoff = sg.npp_gpu("DAM", W, seed=12, rate=rc.inj_rate)
+    ao, bo, uo = (x.cpu().numpy() for x in (a["win_off"], b["win_off"], uoff))
+    att = a["attack"].cpu().numpy()
+    assert att.any() and (~att.astype(bool)).any()
+    for w in range(W):
+        ta = a["t"][ao[w]:ao[w + 1]].cpu().numpy(); ma = a["mark"][ao[w]:ao[w + 1]].cpu().numpy()
+        tb = b["t"][bo[w]:bo[w + 1]].cpu().numpy(); mb = b["mark"][bo[w]:bo[w + 1]].cpu().numpy()
+        if not att[w]:
+            assert np.array_equal(ta, tb) and np.array_equal(ma, mb)
+            continue
+        ti = u[uoff[w]:uoff[w + 1]].cpu().numpy() * rc.T
+        assert len(ta) == len(tb) + len(ti)
+        assert np.all(np.diff(ta) >= 0)
+        merged = np.sort(np.concatenate([tb, ti]), kind="stable")
+        assert np.array_equal(ta, merged)
+        inj = np.isin(ta, ti)
+        assert len(set(ma[inj].tolist())) == 1
