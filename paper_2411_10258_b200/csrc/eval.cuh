@@ -162,6 +162,13 @@ __device__ __forceinline__ float fsel_eqi(int x, int y, float a, float b) {
   return r;
 }
 
+// 1.0f if x == 0 else 0.0f, as one FSET (a select of -1/0 compiles to SEL + I2FP)
+__device__ __forceinline__ float fset_eq0(float x) {
+  float r;
+  asm("set.eq.f32.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // One chunk of 8 events (see event_loop).
 template <int DP, bool GRAD>
 __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __restrict__ A,
@@ -194,8 +201,9 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     const float dr = t - last;
     const float er = ex2f(ar.y * (dr * -kLog2e));
     const float ec = ex2f(bc * (dc * -kLog2e));
-    const float R = fmaf(er, sr.x, fsel_eqf(dr, 0.0f, -1.0f, 0.0f));  // strict T_j^k < t
-    const float p = fmaf(ar.x, R, fsel_eqi(i, j, th, 0.0f));   // theta_i enters through lane i
+    const float R = fmaf(er, sr.x, -fset_eq0(dr));   // strict T_j^k < t
+    // theta_i enters after the reduction for DP >= 8 (below), through lane i for DP <= 4
+    const float p = DP >= 8 ? ar.x * R : fmaf(ar.x, R, fsel_eqi(i, j, th, 0.0f));
     colS[i] = make_float2(fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
     last = fsel_eqi(i, j, t, last);
     if constexpr (DP >= 8) {
@@ -219,7 +227,12 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     __syncwarp();
   }
   if constexpr (DP >= 8) {
-    const float lam = reduce_scatter8<DP>(pv, j);
+    // this lane now holds event e's sum over sources; add theta of its mark (0 for a null
+    // event), which lane gbase + mark holds
+    const int e = (j >> (LG - 3)) & 7;
+    const int ie = (int)__byte_perm(e < 4 ? ck.mm.x : ck.mm.y, 0u, 0x4440u | (unsigned)(e & 3));
+    const float the = __shfl_sync(kFull, th, gbase + (ie & (DP - 1)));
+    const float lam = reduce_scatter8<DP>(pv, j) + (ie < DP ? the : 0.0f);
     if ((j & ((DP >> 3) - 1)) == 0) lacc += lg2f(lam);
     if (GRAD) {
       const float w = rcpf(lam);
