@@ -169,7 +169,48 @@ __device__ __forceinline__ float fset_eq0(float x) {
   return r;
 }
 
-// One chunk of 8 events (see event_loop).
+// Shared-memory accesses of the event loop through explicit 32-bit shared addresses: one
+// IMAD/LEA per array per event (the compiler otherwise re-derives (j*RS + i)*8 + base with
+// two or three integer ops).  The state (SQ, G) accesses are volatile with a memory clobber
+// (their order carries the recurrence); the parameter loads (A, constant during an event
+// loop) are plain asm so the compiler may hoist them across the state stores.
+__device__ __forceinline__ float2 lda2(uint32_t a) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ float lda1o(uint32_t a) {
+  float v;
+  asm("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+__device__ __forceinline__ float2 lds2(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ float2 lds2o(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];"
+               : "=f"(v.x), "=f"(v.y) : "r"(a), "n"(OFF) : "memory");
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ float lds1o(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF) : "memory");
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ void sts2o(uint32_t a, float x, float y) {
+  asm volatile("st.shared.v2.f32 [%0+%1], {%2, %3};" ::"r"(a), "n"(OFF), "f"(x), "f"(y)
+               : "memory");
+}
+
+// One chunk of 8 events (see event_loop).  A, SQ, Gs are one group's arrays laid out
+// contiguously (SQ = A + AS, Gs = A + 2 AS; Smem<DP>).
 template <int DP, bool GRAD>
 __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __restrict__ A,
                                               float2* __restrict__ SQ, float2* __restrict__ Gs,
@@ -177,12 +218,13 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
                                               float& last, float& gth, double& lsum) {
   constexpr int RS = DP + 1;
   constexpr int LG = Log2<DP>::v;
-  // per-lane bases: row i of column j at rowA + i*RS, column i of row j at colA + i
-  const float2* rowA = A + j;
-  float2* rowS = SQ + j;
-  const float2* colA = A + j * RS;
-  float2* colS = SQ + j * RS;
-  float2* rowG = Gs + j;
+  constexpr int kSQ = Smem<DP>::AS * 8, kG = 2 * Smem<DP>::AS * 8;   // byte offsets from A
+  MDHP_ASSERT(SQ == A + Smem<DP>::AS && Gs == A + 2 * Smem<DP>::AS);
+  const uint32_t sA = static_cast<uint32_t>(__cvta_generic_to_shared(A));
+  // per-lane bases: row i of column j at rowb + i*RS*8, column i of row j at colb + i*8,
+  // gradient row i of column j at rowb + kG + i*DP*8
+  const uint32_t rowb = sA + 8u * j;
+  const uint32_t colb = sA + 8u * RS * j;
   float pv[8], Rv[8], Qv[8];
   float lacc = 0.0f;
 #pragma unroll
@@ -194,17 +236,21 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
     const int i = (int)__byte_perm(word, 0u, 0x4440u | (unsigned)(s & 3));   // mark (null: DP)
     MDHP_ASSERT(i >= 0 && i <= DP);
-    const float2 ar = rowA[i * RS];
-    const float2 sr = rowS[i * RS];
-    const float bc = colA[i].y;
-    const float2 sc = colS[i];
+    const uint32_t ra = rowb + (uint32_t)i * (8u * RS);
+    const uint32_t ca = colb + ((uint32_t)i << 3);
+    MDHP_ASSERT(ra + kSQ + 8 <= sA + 8u * Smem<DP>::per_group &&
+                ca + kSQ + 8 <= sA + 8u * Smem<DP>::per_group);
+    const float2 ar = lda2(ra);
+    const float2 sr = lds2o<kSQ>(ra);
+    const float bc = lda1o<4>(ca);
+    const float2 sc = lds2o<kSQ>(ca);
     const float dr = t - last;
     const float er = ex2f(ar.y * (dr * -kLog2e));
     const float ec = ex2f(bc * (dc * -kLog2e));
     const float R = fmaf(er, sr.x, -fset_eq0(dr));   // strict T_j^k < t
     // theta_i enters after the reduction for DP >= 8 (below), through lane i for DP <= 4
     const float p = DP >= 8 ? ar.x * R : fmaf(ar.x, R, fsel_eqi(i, j, th, 0.0f));
-    colS[i] = make_float2(fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
+    sts2o<kSQ>(ca, fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
     last = fsel_eqi(i, j, t, last);
     if constexpr (DP >= 8) {
       pv[s] = p;
@@ -216,10 +262,10 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
       const float lam = group_sum<DP>(p);
       if (GRAD) {
         const float w = rcpf(lam);
-        float2 gg = rowG[i * DP];
-        gg.x = fmaf(R, w, gg.x);
-        gg.y = fmaf(er * fmaf(dr, sr.x, sr.y), w, gg.y);
-        rowG[i * DP] = gg;
+        const uint32_t ga = rowb + ((uint32_t)i * (8u * DP));
+        MDHP_ASSERT(ga + kG + 8 <= sA + 8u * Smem<DP>::per_group);
+        const float2 gg = lds2o<kG>(ga);
+        sts2o<kG>(ga, fmaf(R, w, gg.x), fmaf(er * fmaf(dr, sr.x, sr.y), w, gg.y));
         gth += fsel_eqi(i, j, w, 0.0f);
       }
       lacc += (j == 0) ? lg2f(lam) : 0.0f;
@@ -240,12 +286,15 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
       for (int s = 0; s < 8; s++) {
         const float ws = __shfl_sync(kFull, w, gbase + (s << (LG - 3)));
         const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
-        const int i = (int)__byte_perm(word, 0u, 0x4440u | (unsigned)(s & 3));
+        // re-extract the mark (shift/mask, not pass 1's PRMT) so that pass 1's 8 "i == j"
+        // predicates are not kept live across the reduction (ptxas would pack them into a
+        // register with two LOP3 each)
+        const int i = (int)((word >> (8 * (s & 3))) & 0xffu);
         MDHP_ASSERT(i >= 0 && i <= DP);
-        float2 gg = rowG[i * DP];
-        gg.x = fmaf(Rv[s], ws, gg.x);
-        gg.y = fmaf(Qv[s], ws, gg.y);
-        rowG[i * DP] = gg;
+        const uint32_t ga = (rowb + kG) + ((uint32_t)i << (3 + LG));
+        MDHP_ASSERT(ga >= sA + kG && ga + 8 <= sA + 8u * Smem<DP>::per_group);
+        const float2 gg = lds2(ga);
+        sts2o<0>(ga, fmaf(Rv[s], ws, gg.x), fmaf(Qv[s], ws, gg.y));
         gth += fsel_eqi(i, j, ws, 0.0f);
       }
     }
