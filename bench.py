@@ -462,14 +462,17 @@ def main():
         bi = sum(x.numel() * x.element_size() for x in (t_h, m_h, o_h, T_h, th_h, al_h, be_h))
         bo = (th_h.numel() + al_h.numel() + be_h.numel()) * 4 + W * (8 + 4 + 4)
         ths, als, bes = th_h.clone().pin_memory(), al_h.clone().pin_memory(), be_h.clone().pin_memory()
-        ke = 1   # the kernels are already warm from the device-resident steps above
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
+        ke = 1   # one untimed warm-up call (workspace pool), then ke timed calls
+        M.fit_host(D, t_h, m_h, o_h, T_h, ths, als, bes, cfg, time_mode=1)
+        dt = 0.0
         for _ in range(ke):
-            ths.copy_(th_h); als.copy_(al_h); bes.copy_(be_h)
+            ths.copy_(th_h); als.copy_(al_h); bes.copy_(be_h)   # reset the init (host, untimed)
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
             M.fit_host(D, t_h, m_h, o_h, T_h, ths, als, bes, cfg, time_mode=1)
-        dt = (time.perf_counter() - t0) / ke
+            dt += time.perf_counter() - t0
+        dt /= ke
         dtt = torch.tensor([dt], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(dtt, op=dist.ReduceOp.MAX)

@@ -199,6 +199,9 @@ int mdhp_fit(const mdhp_pack_desc* desc, const void* packed, const mdhp_fit_conf
  * copies the CSR batch and initial parameters to the device, packs, fits, and copies the
  * fitted parameters, loglik, iters and status back.  Same arguments as pack + fit with host
  * pointers.  Synchronous (returns after the device->host copies completed).
+ * Workspace comes from the device's default stream-ordered memory pool; mdhp_fit and
+ * mdhp_fit_host raise that pool's release threshold (once per device) so repeated calls reuse
+ * the memory instead of re-mapping it (cudaMemPoolTrimTo releases it).
  */
 int mdhp_fit_host(const mdhp_pack_desc* desc, const double* t_host, const int32_t* mark_host,
                   const int64_t* win_off_host, const double* T_host,

@@ -234,6 +234,21 @@ int mdhp_loglik_dense(const mdhp_pack_desc* d, const void* packed, const float* 
   return check_cuda("mdhp_loglik_dense");
 }
 
+// Raise the release threshold of the current device's default memory pool (once per device)
+// so that the stream-ordered workspaces of repeated calls are reused instead of being unmapped
+// and re-mapped at every synchronisation (tens of GB for mdhp_fit_host at cfg5 scale).
+static void keep_pool_memory() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 int mdhp_hawkes_features(int32_t D, int64_t W, int32_t H, const float* theta,
                          const float* alpha, const float* beta, const float* T_span,
                          const float* A, const float* B, const float* C, float* hks,
@@ -279,6 +294,7 @@ int mdhp_fit(const mdhp_pack_desc* d, const void* packed, const mdhp_fit_config*
   if (W == 0) return MDHP_OK;
   const size_t PP = (size_t)d->D + 2 * (size_t)d->D * d->D;
   // workspace: work counter (+ zero-initialised Adam moments when the caller passes none)
+  keep_pool_memory();
   const bool own_opt = opt_state == nullptr && cfg->optimizer == MDHP_OPT_ADAM;
   size_t ws_bytes = 256 + (own_opt ? sizeof(float) * 2 * PP * (size_t)W : 0);
   void* ws = nullptr;
@@ -495,6 +511,7 @@ int mdhp_fit_host(const mdhp_pack_desc* d, const double* t_h, const int32_t* mar
     return MDHP_EINVAL;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  keep_pool_memory();
   const int64_t W = d->n_windows, E = d->n_events;
   const int D = d->D;
   const size_t pk = make_layout(D, W, E).total;
