@@ -53,6 +53,28 @@ struct Smem {
   static constexpr size_t per_warp = (size_t)G * per_group * sizeof(float2);
 };
 
+// Parameter pair order in A.  For DP <= 16 the upper half-warp (lanes 16-31, whole groups)
+// stores {beta, alpha} instead of {alpha, beta}: the 32-bit beta column read of the event loop
+// then hits even banks in one half-warp and odd banks in the other (one wavefront instead of
+// two; measured 7% of all shared wavefronts), for two selects per event in the row read.
+// Every access to A goes through these helpers.
+template <int DP>
+__device__ __forceinline__ bool ab_swapped() {
+  return DP <= 16 && (threadIdx.x & 16) != 0;
+}
+template <int DP>
+__device__ __forceinline__ float2 ab_pack(float a, float b) {
+  return ab_swapped<DP>() ? make_float2(b, a) : make_float2(a, b);
+}
+template <int DP>
+__device__ __forceinline__ float ab_alpha(float2 k) {
+  return ab_swapped<DP>() ? k.y : k.x;
+}
+template <int DP>
+__device__ __forceinline__ float ab_beta(float2 k) {
+  return ab_swapped<DP>() ? k.x : k.y;
+}
+
 // The null dimension DP.  A padding slot or the tail of a shorter window in the warp is the
 // event (t = -2, gap 0, mark DP).  With row DP = {alpha, beta} = {1, 0} at column 0 and {0, 0}
 // elsewhere, S_DP,0 = 1 and column DP's beta = 0, such an event reads lambda = 1 exactly
@@ -225,6 +247,8 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
   // gradient row i of column j at rowb + kG + i*DP*8
   const uint32_t rowb = sA + 8u * j;
   const uint32_t colb = sA + 8u * RS * j;
+  // beta of a column pair: word 1, or word 0 where the pair is stored swapped
+  const uint32_t colbb = colb + (ab_swapped<DP>() ? 0u : 4u);
   float pv[8], Rv[8], Qv[8];
   float lacc = 0.0f;
 #pragma unroll
@@ -239,17 +263,18 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     const uint32_t ra = rowb + (uint32_t)i * (8u * RS);
     const uint32_t ca = colb + ((uint32_t)i << 3);
     MDHP_ASSERT(ra + kSQ + 8 <= sA + 8u * Smem<DP>::per_group &&
-                ca + kSQ + 8 <= sA + 8u * Smem<DP>::per_group);
+                ca + kSQ + 4 <= sA + 8u * Smem<DP>::per_group);
     const float2 ar = lda2(ra);
     const float2 sr = lds2o<kSQ>(ra);
-    const float bc = lda1o<4>(ca);
+    const float bc = lda1o<0>(colbb + ((uint32_t)i << 3));
     const float2 sc = lds2o<kSQ>(ca);
     const float dr = t - last;
-    const float er = ex2f(ar.y * (dr * -kLog2e));
+    const float a_ij = ab_alpha<DP>(ar), b_ij = ab_beta<DP>(ar);
+    const float er = ex2f(b_ij * (dr * -kLog2e));
     const float ec = ex2f(bc * (dc * -kLog2e));
     const float R = fmaf(er, sr.x, -fset_eq0(dr));   // strict T_j^k < t
     // theta_i enters after the reduction for DP >= 8 (below), through lane i for DP <= 4
-    const float p = DP >= 8 ? ar.x * R : fmaf(ar.x, R, fsel_eqi(i, j, th, 0.0f));
+    const float p = DP >= 8 ? a_ij * R : fmaf(a_ij, R, fsel_eqi(i, j, th, 0.0f));
     sts2o<kSQ>(ca, fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
     last = fsel_eqi(i, j, t, last);
     if constexpr (DP >= 8) {
