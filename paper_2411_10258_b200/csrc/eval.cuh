@@ -225,6 +225,15 @@ __device__ __forceinline__ float lds1o(uint32_t a) {
   asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF) : "memory");
   return v;
 }
+__device__ __forceinline__ void sts1(uint32_t a, float x) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(x) : "memory");
+}
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
 template <int OFF>
 __device__ __forceinline__ void sts2o(uint32_t a, float x, float y) {
   asm volatile("st.shared.v2.f32 [%0+%1], {%2, %3};" ::"r"(a), "n"(OFF), "f"(x), "f"(y)
@@ -307,9 +316,24 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     if ((j & ((DP >> 3) - 1)) == 0) lacc += lg2f(lam);
     if (GRAD) {
       const float w = rcpf(lam);
+      // broadcast the 8 weights through shared memory (one store + two broadcast loads = 3
+      // slots) instead of 8 shuffles: shuffles and shared wavefronts share one slot per clock
+      // (profiles/r01_ubench_b200.txt).  Scratch: the never-read null row of G (null events of
+      // this chunk overwrite it in the pass below, after it has been read).
+      // (DP <= 16; for DP = 32, one window per warp, the shuffles measured faster).
+      float4 wa = make_float4(0.f, 0.f, 0.f, 0.f), wb = wa;
+      if constexpr (DP <= 16) {
+        const uint32_t scr = sA + kG + 8u * DP * DP;
+        if ((j & ((DP >> 3) - 1)) == 0) sts1(scr + 4u * e, w);
+        __syncwarp();
+        wa = lds4(scr);
+        wb = lds4(scr + 16u);
+      }
 #pragma unroll
       for (int s = 0; s < 8; s++) {
-        const float ws = __shfl_sync(kFull, w, gbase + (s << (LG - 3)));
+        const float ws = DP > 16 ? __shfl_sync(kFull, w, gbase + (s << (LG - 3)))
+                       : s == 0 ? wa.x : s == 1 ? wa.y : s == 2 ? wa.z : s == 3 ? wa.w
+                       : s == 4 ? wb.x : s == 5 ? wb.y : s == 6 ? wb.z : wb.w;
         const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
         // re-extract the mark (shift/mask, not pass 1's PRMT) so that pass 1's 8 "i == j"
         // predicates are not kept live across the reduction (ptxas would pack them into a

@@ -52,6 +52,45 @@ __global__ void k_shfl(float* out, int iters){
   if(a[0]+a[1]+a[2]+a[3]==1.2345f) out[0]=a[0];
 }
 
+// Mixed shared-memory loads and shuffles: do they share one issue resource (MIO/crossbar)?
+// NL LDS.64 and NS SHFL per iteration, independent chains.
+template <int NL, int NS>
+__global__ void k_mix(float* out, int iters){
+  extern __shared__ float2 sm2[];
+  int tid = threadIdx.x;
+  for(int i=tid;i<8192;i+=blockDim.x) sm2[i]=make_float2(i,i);
+  __syncthreads();
+  float2 acc = make_float2(0,0);
+  float a[8]; for(int i=0;i<8;i++) a[i]=tid+i;
+  int lane = tid & 31, w = tid>>5;
+  for(int it=0; it<iters; it++){
+    #pragma unroll
+    for(int u=0;u<NL;u++){
+      float2 v = sm2[((it*8+u)*37 + w*64 + lane) & 8191];
+      acc.x+=v.x; acc.y+=v.y;
+    }
+    #pragma unroll
+    for(int u=0;u<NS;u++) a[u&7] += __shfl_xor_sync(0xffffffffu, a[u&7], 1+(u&3));
+  }
+  float s=acc.x+acc.y; for(int i=0;i<8;i++) s+=a[i];
+  if(s==1.2345f) out[0]=s;
+}
+
+template <int NL, int NS>
+static int run_mix(float* out, int sms, int iters, cudaEvent_t e0, cudaEvent_t e1){
+  CK(cudaFuncSetAttribute(k_mix<NL,NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+  for(int rep=0;rep<2;rep++){
+    cudaEventRecord(e0);
+    k_mix<NL,NS><<<sms*2, 1024, 65536>>>(out, iters);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms,e0,e1);
+    double warp_it = (double)sms*2*1024/32*iters;
+    if(rep==1) printf("mix LDS.64 x%d + SHFL x%d per iter: %.3f ms, clk per warp-iter per SM %.3f\n", NL, NS, ms,
+                      ms*1e6*1.965/ (warp_it/sms));
+  }
+  return 0;
+}
+
 int main(){
   int dev=0; cudaDeviceProp p; CK(cudaGetDeviceProperties(&p,dev));
   int sms = p.multiProcessorCount; int clk=0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
@@ -90,6 +129,10 @@ int main(){
     double ops = (double)sms*8*256/32*iters*4;
     if(rep==1) printf("shfl: %.3f ms, warp-shfl per SM per ns %.3f\n", ms, ops/ms/1e6/sms);
   }
+  run_mix<8,0>(out, sms, iters, e0, e1);
+  run_mix<0,8>(out, sms, iters, e0, e1);
+  run_mix<8,8>(out, sms, iters, e0, e1);
+  run_mix<8,2>(out, sms, iters, e0, e1);
   CK(cudaGetLastError());
   return 0;
 }
