@@ -53,26 +53,30 @@ struct Smem {
   static constexpr size_t per_warp = (size_t)G * per_group * sizeof(float2);
 };
 
-// Parameter pair order in A.  For DP <= 16 the upper half-warp (lanes 16-31, whole groups)
-// stores {beta, alpha} instead of {alpha, beta}: the 32-bit beta column read of the event loop
-// then hits even banks in one half-warp and odd banks in the other (one wavefront instead of
-// two; measured 7% of all shared wavefronts), for two selects per event in the row read.
-// Every access to A goes through these helpers.
+// Parameter pair order in A.  Half of the pairs are stored {beta, alpha} instead of
+// {alpha, beta}, chosen so that the 32-bit beta column read of the event loop hits even banks
+// in one half-warp and odd banks in the other (one wavefront instead of two; 7% of all shared
+// wavefronts at D = 16) for two selects per event in the row read:
+//   DP <= 16: the upper half-warp (lanes 16-31; whole groups) stores its pairs swapped.
+//   DP == 32 (one window per warp) would have to swap by row (r >= 16), which needs a per-event
+//   predicate in the row read; measured 1% slower on cfg3, so DP = 32 keeps one order.
+// Every access to A goes through these helpers (r = row index of the pair).
 template <int DP>
-__device__ __forceinline__ bool ab_swapped() {
+__device__ __forceinline__ bool ab_swapped(int r) {
+  (void)r;
   return DP <= 16 && (threadIdx.x & 16) != 0;
 }
 template <int DP>
-__device__ __forceinline__ float2 ab_pack(float a, float b) {
-  return ab_swapped<DP>() ? make_float2(b, a) : make_float2(a, b);
+__device__ __forceinline__ float2 ab_pack(int r, float a, float b) {
+  return ab_swapped<DP>(r) ? make_float2(b, a) : make_float2(a, b);
 }
 template <int DP>
-__device__ __forceinline__ float ab_alpha(float2 k) {
-  return ab_swapped<DP>() ? k.y : k.x;
+__device__ __forceinline__ float ab_alpha(int r, float2 k) {
+  return ab_swapped<DP>(r) ? k.y : k.x;
 }
 template <int DP>
-__device__ __forceinline__ float ab_beta(float2 k) {
-  return ab_swapped<DP>() ? k.x : k.y;
+__device__ __forceinline__ float ab_beta(int r, float2 k) {
+  return ab_swapped<DP>(r) ? k.x : k.y;
 }
 
 // The null dimension DP.  A padding slot or the tail of a shorter window in the warp is the
@@ -257,7 +261,7 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
   const uint32_t rowb = sA + 8u * j;
   const uint32_t colb = sA + 8u * RS * j;
   // beta of a column pair: word 1, or word 0 where the pair is stored swapped
-  const uint32_t colbb = colb + (ab_swapped<DP>() ? 0u : 4u);
+  const uint32_t colbb = colb + (ab_swapped<DP>(j) ? 0u : 4u);
   float pv[8], Rv[8], Qv[8];
   float lacc = 0.0f;
 #pragma unroll
@@ -278,7 +282,7 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     const float bc = lda1o<0>(colbb + ((uint32_t)i << 3));
     const float2 sc = lds2o<kSQ>(ca);
     const float dr = t - last;
-    const float a_ij = ab_alpha<DP>(ar), b_ij = ab_beta<DP>(ar);
+    const float a_ij = ab_alpha<DP>(i, ar), b_ij = ab_beta<DP>(i, ar);
     const float er = ex2f(b_ij * (dr * -kLog2e));
     const float ec = ex2f(bc * (dc * -kLog2e));
     const float R = fmaf(er, sr.x, -fset_eq0(dr));   // strict T_j^k < t

@@ -45,7 +45,7 @@ __device__ __forceinline__ double eval_window(const Packed& P, float2* A, float2
     const float2 k = A[i * (DP + 1) + c.j];
     const float2 sq = SQ[i * (DP + 1) + c.j];
     float Eb, Hb2;
-    const float ka = ab_alpha<DP>(k), kb = ab_beta<DP>(k);
+    const float ka = ab_alpha<DP>(i, k), kb = ab_beta<DP>(i, k);
     compensator(cc, S, kb, sq.x, sq.y, Eb, Hb2);
     if (cc.real && i < P.D) {
       part3 += (double)(ka * Eb);
@@ -94,10 +94,10 @@ __device__ __forceinline__ float load_params(float2* A, const WarpCtx<DP>& c, in
       a = alpha[(size_t)w * D * D + (size_t)i * D + c.j];
       b = beta[(size_t)w * D * D + (size_t)i * D + c.j];
     }
-    A[i * (DP + 1) + c.j] = ab_pack<DP>(a, b);
+    A[i * (DP + 1) + c.j] = ab_pack<DP>(i, a, b);
   }
   // null dimension (see eval.cuh): row DP = {1,0} at column 0, column DP has beta = 0
-  A[DP * (DP + 1) + c.j] = ab_pack<DP>(c.j == 0 ? 1.0f : 0.0f, 0.0f);
+  A[DP * (DP + 1) + c.j] = ab_pack<DP>(DP, c.j == 0 ? 1.0f : 0.0f, 0.0f);
   A[c.j * (DP + 1) + DP] = make_float2(0.0f, 0.0f);
   return real ? theta[(size_t)w * D + c.j] : 0.0f;
 }
@@ -179,10 +179,10 @@ __device__ __forceinline__ void step_column(float2* A, const float2* Gs, const W
     float2* k = &A[i * (DP + 1) + c.j];
     const float2 gg = Gs[i * DP + c.j];
     const size_t q = (size_t)D + (size_t)i * D + c.j;
-    float ka = ab_alpha<DP>(*k), kb = ab_beta<DP>(*k);
+    float ka = ab_alpha<DP>(i, *k), kb = ab_beta<DP>(i, *k);
     if (cfg.fit_mask & MDHP_FIT_ALPHA) ka = upd(ka, gg.x, q, 0.0f);
     if (cfg.fit_mask & MDHP_FIT_BETA) kb = upd(kb, gg.y, q + (size_t)D * D, cfg.min_param);
-    *k = ab_pack<DP>(ka, kb);
+    *k = ab_pack<DP>(i, ka, kb);
   }
 }
 
@@ -194,8 +194,8 @@ __device__ __forceinline__ void store_params(const float2* A, const WarpCtx<DP>&
   theta[(size_t)w * D + c.j] = th;
   for (int i = 0; i < D; i++) {
     const float2 k = A[i * (DP + 1) + c.j];
-    alpha[(size_t)w * D * D + (size_t)i * D + c.j] = ab_alpha<DP>(k);
-    beta[(size_t)w * D * D + (size_t)i * D + c.j] = ab_beta<DP>(k);
+    alpha[(size_t)w * D * D + (size_t)i * D + c.j] = ab_alpha<DP>(i, k);
+    beta[(size_t)w * D * D + (size_t)i * D + c.j] = ab_beta<DP>(i, k);
   }
 }
 

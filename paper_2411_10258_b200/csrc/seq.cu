@@ -461,12 +461,12 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
   const size_t DD = (size_t)D * D;
   for (int i = 0; i < DP; i++) {
     const bool real = live && i < D && j < D;
-    A[i * RS + j] = real ? ab_pack<DP>(alpha[(size_t)i * D + j], beta[(size_t)i * D + j])
-                         : ab_pack<DP>(0.0f, 1.0f);
+    A[i * RS + j] = real ? ab_pack<DP>(i, alpha[(size_t)i * D + j], beta[(size_t)i * D + j])
+                         : ab_pack<DP>(i, 0.0f, 1.0f);
     SQ[i * RS + j] = real ? carry[(size_t)c * DD + (size_t)i * D + j] : make_float2(0.0f, 0.0f);
     Gs[i * DP + j] = make_float2(0.0f, 0.0f);
   }
-  A[DP * RS + j] = ab_pack<DP>(j == 0 ? 1.0f : 0.0f, 0.0f);
+  A[DP * RS + j] = ab_pack<DP>(DP, j == 0 ? 1.0f : 0.0f, 0.0f);
   A[j * RS + DP] = make_float2(0.0f, 0.0f);
   SQ[DP * RS + j] = make_float2(j == 0 ? 1.0f : 0.0f, 0.0f);
   SQ[j * RS + DP] = make_float2(0.0f, 0.0f);
