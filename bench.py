@@ -496,6 +496,16 @@ def main():
     Dp = 1 << (D - 1).bit_length()
     smem_bytes = ev_it_step * 52 * Dp
     smem_peak = 148 * 128 * 1.965   # GB/s at clocks.max.sm
+    # the binding pipe of this design: shared-memory wavefronts and warp
+    # shuffles share one MIO slot per clock per SM (profiles/r01_ubench_b200.txt).  Per
+    # event-evaluation: 52*Dp/128 wavefronts + the reduction/broadcast slots per window-event
+    # (per 8-event chunk and warp: reduce-scatter + theta shuffle + weight broadcast, / G*8)
+    shfl_per_ev = {8: 11 / 32, 16: 12 / 16, 32: 18 / 8}.get(Dp, 0.0)
+    mio_per_ev = 52 * Dp / 128 + shfl_per_ev
+    mio_peak = 148 * 1.965   # G slots/s
+    mio_ach = ev_it_step * mio_per_ev / (fit_avg / 1e3) / 1e9
+    mio = {"achieved_Gslots": mio_ach, "peak_Gslots": mio_peak, "frac": mio_ach / mio_peak,
+           "per_unit": f"{mio_per_ev:.3f} MIO slots per event-iteration (shared wavefronts + shuffles)"}
     roof = {"bound": "alu", "achieved": achieved, "peak": MUFU_PEAK_GOPS, "unit": "Gop/s (MUFU)",
             "frac": achieved / MUFU_PEAK_GOPS, "traffic": traffic, "kernel": f"k_fit<{Dp}>",
             "per_unit": f"{mufu_per_ev} MUFU ops per event-iteration (2D ex2 + lg2 + rcp)",
@@ -504,6 +514,7 @@ def main():
             "smem": {"achieved_GBps": smem_bytes / (fit_avg / 1e3) / 1e9, "peak_GBps": smem_peak,
                      "frac": smem_bytes / (fit_avg / 1e3) / 1e9 / smem_peak,
                      "per_unit": f"{52 * Dp} B shared-memory traffic per event-iteration"},
+            "mio": mio,
             "fit_ms_avg": fit_avg, "fit_share_of_step": fit_avg / (ms / args.steps)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
