@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--inject", default="none", choices=["none", "PLA", "DEA", "ASA", "DAM"],
                     help="time-exciting injections (Table II + Algorithm 4) in attack windows (row f2)")
+    ap.add_argument("--chunk", type=int, default=256, help="--config cfg4: events per chunk")
     ap.add_argument("--hidden", type=int, default=128, help="--config feat: MDHP-LSTM hidden size H")
     ap.add_argument("--shard-seq", action="store_true",
                     help="cfg4: split ONE sequence over the ranks (f1, strong scaling, NCCL map exchange)")
@@ -189,7 +190,7 @@ def bench_seq(args, rc, world, rank, dev):
         return bench_seq_sharded(args, rc, world, rank, dev)
     b = sgpu.make_batch_gpu(rc, 1, seed=args.seed, first_window=rank, device=dev)
     N = int(b["win_off"][-1])
-    ps = M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=256)
+    ps = M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=args.chunk)
     th0 = b["theta"][0].clone(); al0 = b["alpha"][0].clone(); be0 = b["beta"][0].clone()
     th, al, be = th0.clone(), al0.clone(), be0.clone()
     cfg = M.FitConfig(max_iters=args.iters, optimizer="adam", lr=0.05, tol_rel=0.0)
@@ -197,7 +198,7 @@ def bench_seq(args, rc, world, rank, dev):
 
     def step():
         th.copy_(th0); al.copy_(al0); be.copy_(be0)
-        M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=256, out=ps)
+        M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=args.chunk, out=ps)
         return M.seq_fit(ps, th, al, be, cfg)
     for _ in range(args.warmup):
         r = step()
@@ -223,7 +224,7 @@ def bench_seq(args, rc, world, rank, dev):
                           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                           "data": f"synthetic (Ogata-thinned MDHP on GPU, recipe cfg4, seed {args.seed})",
                           "config": {"workload": f"cfg4: one sequence/GPU, D={D}, {N} events over {rc.T}s, "
-                                                 f"chunked scan (256 events/chunk), Adam lr 0.05, {args.iters} "
+                                                 f"chunked scan ({args.chunk} events/chunk), Adam lr 0.05, {args.iters} "
                                                  "fixed iterations + final eval", "events": N},
                           "gpu_launches": int(M.launch_count() - L0)}), flush=True)
     if world > 1:

@@ -146,6 +146,7 @@ struct FitCfgDev {
 
 // launch counter (process-wide), incremented by every launch site
 void count_launch(int k = 1);
+uint64_t launches_so_far();
 void set_error(const char* fmt, ...);
 
 }  // namespace mdhp

@@ -15,6 +15,7 @@
 //                          epilogue from the global final state, and (fit) one optimizer step.
 // Chunk-relative fp32 times (fp64 base per chunk) keep ~1e-7 s resolution over 1000 s.
 #include <cmath>
+#include <cstdlib>
 #include "eval.cuh"
 
 namespace mdhp {
@@ -249,6 +250,8 @@ k_seq_momsum(int Dp, int64_t C, const float* __restrict__ cmom, float* __restric
 }
 
 // ---------------------------------------------------------------- evaluation workspace
+constexpr int kRedBlocks = 512;   // stage-1 blocks of the chunk reduction (phase 4a)
+
 struct SeqWork {
   float2* loc;     // [C][D*D]  local state at chunk end (target-major pairs)
   float2* carry;   // [C][D*D]  state carried into the chunk, anchored at its base
@@ -276,7 +279,7 @@ inline SeqWork make_seq_work(void* base, int D, int Dp, int64_t C) {
                h = take(sizeof(float) * C * Dp), l = take(sizeof(double) * (C + 1)),
                gs = take(sizeof(float2) * DD), gt = take(sizeof(float) * Dp), ls = take(sizeof(double)),
                ct = take(sizeof(int) * 64), pv = take(sizeof(float) * P), op = take(sizeof(float) * 2 * P),
-               rp = take(sizeof(double) * 128 * (2 * DD + D + 1));
+               rp = take(sizeof(double) * kRedBlocks * (2 * DD + D + 1));
   char* B = static_cast<char*>(base);
   w.loc = reinterpret_cast<float2*>(B + a);
   w.carry = reinterpret_cast<float2*>(B + b);
@@ -325,24 +328,43 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
     SQ[j * RS + i] = make_float2(0.0f, 0.0f);
     B[j * RS + i] = (j < D && i < D) ? beta[(size_t)j * D + i] : 0.0f;   // beta_ji: row j, col i
   }
+  // column DP: the null event's (never read) column
+  SQ[j * RS + DP] = make_float2(0.0f, 0.0f);
+  B[j * RS + DP] = 0.0f;
   __syncwarp();
   int nmax = n;
   for (int o = 16; o >= 1; o >>= 1) nmax = max(nmax, __shfl_xor_sync(kFull, nmax, o));
   const int64_t beg = live ? cbeg[c] : 0;
   float last = -1.0f;
-  for (int k = 0; k < nmax; k++) {
-    const bool act = k < n;
-    const float t = act ? t32[beg + k] : 0.0f;
-    const float dc = act ? dtp[beg + k] : 0.0f;
-    const int i = act ? (int)mk[beg + k] : 0;
-    MDHP_ASSERT(i >= 0 && i < DP);
-    if (act) {
-      const float2 s = SQ[j * RS + i];
+  // 8 events per vector load (the chunk layout is the window layout: 8-aligned, padded with
+  // null events up to a multiple of 8 plus one null chunk), the next chunk prefetched
+  const float* tw = t32 + beg;
+  const float* dw = dtp + beg;
+  const uint8_t* mw = mk + beg;
+  const int npad = (n + 7) & ~7;
+  auto local8 = [&](const Chunk& ck) {
+#pragma unroll
+    for (int s = 0; s < 8; s++) {
+      const float t = s == 0 ? ck.ta.x : s == 1 ? ck.ta.y : s == 2 ? ck.ta.z : s == 3 ? ck.ta.w
+                    : s == 4 ? ck.tb.x : s == 5 ? ck.tb.y : s == 6 ? ck.tb.z : ck.tb.w;
+      const float dc = s == 0 ? ck.da.x : s == 1 ? ck.da.y : s == 2 ? ck.da.z : s == 3 ? ck.da.w
+                     : s == 4 ? ck.db.x : s == 5 ? ck.db.y : s == 6 ? ck.db.z : ck.db.w;
+      const int i = (int)__byte_perm(s < 4 ? ck.mm.x : ck.mm.y, 0u, 0x4440u | (unsigned)(s & 3));
+      MDHP_ASSERT(i >= 0 && i <= DP);   // DP: null event (gap 0, beta 0: a no-op on column DP)
+      const float2 sv = SQ[j * RS + i];
       const float e = ex2f(B[j * RS + i] * (dc * -kLog2e));
-      SQ[j * RS + i] = make_float2(fmaf(e, s.x, 1.0f), e * fmaf(dc, s.x, s.y));
-      if (i == j) last = t;
+      SQ[j * RS + i] = make_float2(fmaf(e, sv.x, 1.0f), e * fmaf(dc, sv.x, sv.y));
+      last = fsel_eqi(i, j, t, last);
+      __syncwarp();
     }
-    __syncwarp();
+  };
+  Chunk c0, c1;
+  load_chunk(c0, tw, dw, mw, 0 < n ? 0 : npad);
+  for (int base = 0; base < nmax; base += 16) {
+    load_chunk(c1, tw, dw, mw, min(base + 8, npad));
+    local8(c0);
+    load_chunk(c0, tw, dw, mw, min(base + 16, npad));
+    local8(c1);
   }
   const float Lc = live ? cspan[c] : 0.0f;
   for (int i = 0; i < DP; i++) {
@@ -500,7 +522,6 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
 // 2 D^2 gradient accumulators, D g_theta sums, 1 lsum.  Stage 1: block b sums its contiguous
 // range of chunks for every element (threads over elements: coalesced rows); stage 2: one block
 // sums the kRedBlocks partials per element.
-constexpr int kRedBlocks = 128;
 
 __global__ void __launch_bounds__(256)
 k_seq_reduce1(int D, int Dp, int64_t C, const float2* __restrict__ gpart,
@@ -514,8 +535,18 @@ k_seq_reduce1(int D, int Dp, int64_t C, const float2* __restrict__ gpart,
     double acc = 0.0;
     if (e < 2 * DD) {
       if (grad) {
+        // chunks in order; the loads are independent (unrolled), the adds stay in order
         const float* gp = reinterpret_cast<const float*>(gpart);
-        for (int64_t c = c0; c < c1; c++) acc += (double)gp[c * 2 * DD + e];
+        int64_t c = c0;
+        for (; c + 4 <= c1; c += 4) {
+          const float v0 = gp[c * 2 * DD + e], v1 = gp[(c + 1) * 2 * DD + e];
+          const float v2 = gp[(c + 2) * 2 * DD + e], v3 = gp[(c + 3) * 2 * DD + e];
+          acc += (double)v0;
+          acc += (double)v1;
+          acc += (double)v2;
+          acc += (double)v3;
+        }
+        for (; c < c1; c++) acc += (double)gp[c * 2 * DD + e];
       }
     } else if (e < 2 * DD + D) {
       if (grad)
@@ -527,23 +558,28 @@ k_seq_reduce1(int D, int Dp, int64_t C, const float2* __restrict__ gpart,
   }
 }
 
-__global__ void __launch_bounds__(1024)
+// Stage 2: one warp per element; lane l sums partials l, l+32, ... in order, then a fixed
+// xor-butterfly combines the 32 lane sums (deterministic: the order never depends on timing).
+__global__ void __launch_bounds__(256)
 k_seq_reduce2(int D, const double* __restrict__ part, float2* __restrict__ gsum,
               float* __restrict__ gth, double* __restrict__ ls, int grad, const int* __restrict__ ctl,
               double* __restrict__ raw) {
   if (ctl && ctl[0] == 1 && grad) return;
   const int DD = D * D, NE = 2 * DD + D + 1;
-  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
-    double acc = 0.0;
-    for (int q = 0; q < kRedBlocks; q++) acc += part[(size_t)q * NE + e];
-    if (raw) raw[e] = acc;   // f1: the slice's exact partial sums, all-reduced across ranks
-    if (e < 2 * DD) {
-      if (grad) reinterpret_cast<float*>(gsum)[e] = (float)acc;
-    } else if (e < 2 * DD + D) {
-      if (grad) gth[e - 2 * DD] = (float)acc;
-    } else {
-      ls[0] = acc;
-    }
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (e >= NE) return;
+  double acc = 0.0;
+#pragma unroll 4
+  for (int q = lane; q < kRedBlocks; q += 32) acc += part[(size_t)q * NE + e];
+  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  if (lane != 0) return;
+  if (raw) raw[e] = acc;   // f1: the slice's exact partial sums, all-reduced across ranks
+  if (e < 2 * DD) {
+    if (grad) reinterpret_cast<float*>(gsum)[e] = (float)acc;
+  } else if (e < 2 * DD + D) {
+    if (grad) gth[e - 2 * DD] = (float)acc;
+  } else {
+    ls[0] = acc;
   }
 }
 
@@ -793,7 +829,6 @@ static void seq_phases_t(const SeqLayout& L, const void* pk, const float* th, co
   constexpr int G = 32 / DP;
   const unsigned blk = (unsigned)((C + 4 * G - 1) / (4 * G));
   const size_t lsm = (size_t)4 * G * DP * (DP + 1) * (sizeof(float2) + sizeof(float));
-  cudaFuncSetAttribute(k_seq_local<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
   if (!sd.skip_local) {
     k_seq_local<DP><<<blk, 128, lsm, st>>>(L.D, C, at<int64_t>(pk, L.cstart), at<int64_t>(pk, L.cbeg),
                                          at<float>(pk, L.cspan), at<float>(pk, L.t32),
@@ -809,7 +844,6 @@ static void seq_phases_t(const SeqLayout& L, const void* pk, const float* th, co
   const int has_history = sd.has_history;
   using SM = Smem<DP>;
   const size_t smem = 4 * SM::per_warp;
-  cudaFuncSetAttribute(k_seq_eval<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_seq_eval<DP><<<blk, 128, smem, st>>>(L.D, C, at<int64_t>(pk, L.cstart), at<int64_t>(pk, L.cbeg),
                                          at<float>(pk, L.t32), at<float>(pk, L.dtp),
                                          at<uint8_t>(pk, L.mark), th, al, be, w.carry, w.gpart,
@@ -817,9 +851,36 @@ static void seq_phases_t(const SeqLayout& L, const void* pk, const float* th, co
   count_launch();
 }
 
+// Dynamic shared-memory limits of the phase kernels (host-side; done before a graph capture).
+template <int DP>
+static void seq_set_attrs_t() {
+  constexpr int G = 32 / DP;
+  const size_t lsm = (size_t)4 * G * DP * (DP + 1) * (sizeof(float2) + sizeof(float));
+  cudaFuncSetAttribute(k_seq_local<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
+  cudaFuncSetAttribute(k_seq_eval<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(4 * Smem<DP>::per_warp));
+}
+
+static void seq_set_attrs(const SeqLayout& L) {
+  static bool done[6] = {};
+  int k = 0;
+  while ((1 << k) < L.Dp && k < 5) k++;
+  if (done[k]) return;
+  done[k] = true;
+  switch (L.Dp) {
+    case 1: seq_set_attrs_t<1>(); break;
+    case 2: seq_set_attrs_t<2>(); break;
+    case 4: seq_set_attrs_t<4>(); break;
+    case 8: seq_set_attrs_t<8>(); break;
+    case 16: seq_set_attrs_t<16>(); break;
+    case 32: seq_set_attrs_t<32>(); break;
+  }
+}
+
 static void seq_phases(const SeqLayout& L, const void* pk, const float* th, const float* al,
                        const float* be, const SeqWork& w, int grad, const int* ctl,
                        cudaStream_t st, const SeqDist& sd = SeqDist()) {
+  seq_set_attrs(L);   // once per Dp per process (before any graph capture, see seq_fit_launch)
   switch (L.Dp) {
     case 1: seq_phases_t<1>(L, pk, th, al, be, w, grad, ctl, st, sd); break;
     case 2: seq_phases_t<2>(L, pk, th, al, be, w, grad, ctl, st, sd); break;
@@ -835,7 +896,8 @@ static void seq_reduce(const SeqLayout& L, const SeqWork& w, int grad, const int
   if (L.C == 0) return;
   k_seq_reduce1<<<kRedBlocks, 256, 0, st>>>(L.D, L.Dp, L.C, w.gpart, w.gthp, w.lsp, w.rpart, grad,
                                             ctl);
-  k_seq_reduce2<<<1, 1024, 0, st>>>(L.D, w.rpart, w.gsum, w.gth, w.ls, grad, ctl, raw);
+  const int ne = 2 * L.D * L.D + L.D + 1;
+  k_seq_reduce2<<<(ne + 7) / 8, 256, 0, st>>>(L.D, w.rpart, w.gsum, w.gth, w.ls, grad, ctl, raw);
   count_launch(2);
 }
 
@@ -892,15 +954,48 @@ int seq_fit_launch(int D, int64_t N, int ce, double T, const void* pk, const Fit
   k_seq_gate<<<1, 1, 0, st>>>(at<const int32_t>(pk, L.status), w.ctl, status);
   count_launch(1);
   if (trace) cudaMemsetAsync(trace, 0xff, sizeof(float) * (size_t)(cfg.max_iters > 0 ? cfg.max_iters : 1), st);
-  for (int it = 0; it < cfg.max_iters; it++) {
-    seq_phases(L, pk, th, al, be, w, 1, w.ctl, st);
-    seq_reduce(L, w, 1, w.ctl, st);
-    k_seq_finish<<<1, 1024, 0, st>>>(D, L.Dp, T, at<float>(pk, L.tail), at<int32_t>(pk, L.cnt),
-                                     at<float>(pk, L.umax), at<float>(pk, L.mom), w.fin, w.gsum,
-                                     w.gth, w.ls, th, al, be, lnl, nullptr, nullptr, nullptr, 1,
-                                     w.ctl, cfg, w.prev, opt, trace, N, status, iters,
-                                     at<int32_t>(pk, L.status));
+  // one iteration = phases 1-3 + the two-stage reduction + finish (6 kernels), gated on the
+  // device by the control block, so the host loop never reads back: it is captured once as a
+  // CUDA graph and replayed max_iters times (MDHP_NO_GRAPH=1 launches the kernels directly)
+  auto iteration = [&](cudaStream_t s) {
+    seq_phases(L, pk, th, al, be, w, 1, w.ctl, s);
+    seq_reduce(L, w, 1, w.ctl, s);
+    k_seq_finish<<<1, 1024, 0, s>>>(D, L.Dp, T, at<float>(pk, L.tail), at<int32_t>(pk, L.cnt),
+                                    at<float>(pk, L.umax), at<float>(pk, L.mom), w.fin, w.gsum,
+                                    w.gth, w.ls, th, al, be, lnl, nullptr, nullptr, nullptr, 1,
+                                    w.ctl, cfg, w.prev, opt, trace, N, status, iters,
+                                    at<int32_t>(pk, L.status));
     count_launch(1);
+  };
+  const char* ng = getenv("MDHP_NO_GRAPH");
+  if (cfg.max_iters > 1 && !(ng && ng[0] && ng[0] != '0')) {
+    seq_set_attrs(L);
+    // capture on a private stream (the caller's may be the legacy default stream, which
+    // cannot be captured); the graph is then launched on the caller's stream
+    cudaStream_t cs = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess;
+    const uint64_t before = launches_so_far();
+    ok = ok && cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      iteration(cs);
+      ok = cudaStreamEndCapture(cs, &g) == cudaSuccess && g != nullptr;
+    }
+    const int per_it = (int)(launches_so_far() - before);
+    ok = ok && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+    for (int it = 0; it < cfg.max_iters && ok; it++) ok = cudaGraphLaunch(ge, st) == cudaSuccess;
+    if (ok) count_launch(per_it * (cfg.max_iters - 1));   // the capture counted one iteration
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    if (cs) cudaStreamDestroy(cs);
+    if (!ok) {
+      set_error("seq fit: CUDA graph capture/launch failed: %s",
+                cudaGetErrorString(cudaGetLastError()));
+      rc = MDHP_ECUDA;
+    }
+  } else {
+    for (int it = 0; it < cfg.max_iters; it++) iteration(st);
   }
   // lnL at the returned point
   seq_phases(L, pk, th, al, be, w, 0, nullptr, st);
