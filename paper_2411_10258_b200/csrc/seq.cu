@@ -21,7 +21,6 @@
 namespace mdhp {
 
 constexpr int kSeqWPB = 4;
-constexpr int kScanSeg = 256;
 
 struct SeqLayout {
   int D, Dp;
@@ -383,10 +382,11 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
   }
 }
 
-// Phase 2: exclusive scan of the per-chunk affine maps, one block per pair, kScanSeg segments.
-// A map over a stretch of span L is x -> (E S + Sb, E (Q + L S) + Qb), E = e^{-beta L};
-// composing "m1 then m2" gives E = E2 E1, L = L1 + L2, Sb = E2 Sb1 + Sb2,
-// Qb = E2 (Qb1 + L2 Sb1) + Qb2 (associative), so segments are scanned in log2(kScanSeg) rounds.
+// Phase 2: exclusive scan of the per-chunk affine maps.  Block = kScanP pairs x kScanS segments
+// of chunks (thread = (segment, pair), pair fastest: a warp's loads of a chunk's pair row fill
+// whole 32-byte sectors); each thread composes its segment in order, the segment maps are
+// scanned across the block in log2(kScanS) rounds, then each thread re-walks its segment writing
+// the carried states.  (kScanP = 32 with 32 segments was measured 2x slower: too few blocks.)
 struct AffMap {
   float E, L, Sb, Qb;
 };
@@ -399,36 +399,43 @@ __device__ __forceinline__ AffMap compose(const AffMap& m1, const AffMap& m2) {
   return r;
 }
 
-__global__ void __launch_bounds__(kScanSeg)
+constexpr int kScanP = 4, kScanS = 256;   // pairs x segments per scan block (1024 threads)
+
+__global__ void __launch_bounds__(kScanP * kScanS)
 k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __restrict__ beta,
            const float2* __restrict__ loc, float2* __restrict__ carry, float2* __restrict__ fin,
            const int* __restrict__ ctl, const float2* __restrict__ maps,
            const float* __restrict__ spans, int rank, float2* __restrict__ rankmap,
            float* __restrict__ rankspan, int maps_only) {
   if (ctl && ctl[0]) return;
-  __shared__ AffMap sm[kScanSeg];
-  const int p = blockIdx.x, s = threadIdx.x;
-  const size_t DD = (size_t)D * D;
-  const float b = beta[p];
-  const int64_t per = (C + kScanSeg - 1) / kScanSeg;
-  const int64_t c0 = min(C, (int64_t)s * per), c1 = min(C, c0 + per);
+  __shared__ AffMap sm[kScanS][kScanP];
+  const int lane = threadIdx.x % kScanP, seg = threadIdx.x / kScanP;
+  const int64_t DD = (int64_t)D * D;
+  const int64_t p = (int64_t)blockIdx.x * kScanP + lane;
+  const bool valid = p < DD;
+  const float b = valid ? beta[p] : 0.0f;
+  const int64_t per = (C + kScanS - 1) / kScanS;
+  const int64_t c0 = min(C, (int64_t)seg * per), c1 = min(C, c0 + per);
   AffMap m{1.0f, 0.0f, 0.0f, 0.0f};
-  for (int64_t c = c0; c < c1; c++) {
-    const float L = cspan[c];
-    const float2 l = loc[c * DD + p];
-    const AffMap mc{ex2f(b * (L * -kLog2e)), L, l.x, l.y};
-    m = compose(m, mc);
+  if (valid) {
+    for (int64_t c = c0; c < c1; c++) {
+      const float L = cspan[c];
+      const float2 l = loc[c * DD + p];
+      const AffMap mc{ex2f(b * (L * -kLog2e)), L, l.x, l.y};
+      m = compose(m, mc);
+    }
   }
-  sm[s] = m;
+  sm[seg][lane] = m;
   __syncthreads();
-  for (int o = 1; o < kScanSeg; o <<= 1) {   // inclusive Hillis-Steele scan of the maps
+  for (int o = 1; o < kScanS; o <<= 1) {   // inclusive Hillis-Steele scan over the segments
     AffMap prev = m;
-    if (s >= o) prev = compose(sm[s - o], m);
+    if (seg >= o) prev = compose(sm[seg - o][lane], m);
     __syncthreads();
     m = prev;
-    sm[s] = m;
+    sm[seg][lane] = m;
     __syncthreads();
   }
+  if (!valid) return;
   // state carried into this slice (f1, multi-GPU): the earlier slices' maps composed in order
   float2 x0 = make_float2(0.0f, 0.0f);
   if (maps) {
@@ -442,14 +449,14 @@ k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __res
   auto apply = [&](const AffMap& M, float2 x) {
     return make_float2(fmaf(M.E, x.x, M.Sb), fmaf(M.E, fmaf(M.L, x.x, x.y), M.Qb));
   };
-  if (s == kScanSeg - 1) {
+  if (seg == kScanS - 1) {
     fin[p] = apply(m, x0);
     if (rankmap) rankmap[p] = make_float2(m.Sb, m.Qb);
     if (rankspan && p == 0) rankspan[0] = m.L;
   }
   if (maps_only) return;
-  // state entering segment s = (inclusive map of segment s-1) applied to the carried-in state
-  float2 x = s > 0 ? apply(sm[s - 1], x0) : x0;
+  // state entering segment seg = (inclusive map of segment seg-1) applied to the carried state
+  float2 x = seg > 0 ? apply(sm[seg - 1][lane], x0) : x0;
   for (int64_t c = c0; c < c1; c++) {
     carry[c * DD + p] = x;
     const float L = cspan[c];
@@ -836,7 +843,7 @@ static void seq_phases_t(const SeqLayout& L, const void* pk, const float* th, co
                                          grad ? ctl : nullptr);
     count_launch();
   }
-  k_seq_scan<<<L.D * L.D, kScanSeg, 0, st>>>(L.D, C, at<float>(pk, L.cspan), be, w.loc, w.carry,
+  k_seq_scan<<<(L.D * L.D + kScanP - 1) / kScanP, kScanP * kScanS, 0, st>>>(L.D, C, at<float>(pk, L.cspan), be, w.loc, w.carry,
                                              w.fin, grad ? ctl : nullptr, sd.maps, sd.spans,
                                              sd.rank, sd.rankmap, sd.rankspan, sd.maps_only);
   count_launch();
@@ -1155,8 +1162,9 @@ int seq_parts_launch(int D, int64_t N, int ce, const void* pk, const float* th, 
   if (L.C == 0) {
     // empty slice: no partial sums; its end state is the carried-in state (maps of earlier ranks)
     cudaMemsetAsync(parts, 0, sizeof(double) * (2 * DD + D + 1), st);
-    k_seq_scan<<<D * D, kScanSeg, 0, st>>>(D, 0, nullptr, be, nullptr, nullptr, fin, nullptr, maps,
-                                           spans, rank, nullptr, nullptr, 1);
+    k_seq_scan<<<(D * D + kScanP - 1) / kScanP, kScanP * kScanS, 0, st>>>(D, 0, nullptr, be, nullptr, nullptr, fin,
+                                                          nullptr, maps, spans, rank, nullptr,
+                                                          nullptr, 1);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
   }
