@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--inject", default="none", choices=["none", "PLA", "DEA", "ASA", "DAM"],
                     help="time-exciting injections (Table II + Algorithm 4) in attack windows (row f2)")
+    ap.add_argument("--tol", type=float, default=0.0,
+                    help="converged mode (SURVEY 8(d)): tol_rel (e.g. 1e-6, patience 10, capped at --iters); "
+                         "0 = fixed-iteration mode (the headline)")
     ap.add_argument("--chunk", type=int, default=256, help="--config cfg4: events per chunk")
     ap.add_argument("--hidden", type=int, default=128, help="--config feat: MDHP-LSTM hidden size H")
     ap.add_argument("--shard-seq", action="store_true",
@@ -394,7 +397,7 @@ def main():
     init_al = torch.full((W, D, D), 0.5, device=dev)
     init_be = torch.full((W, D, D), 1.0, device=dev)
     th, al, be = init_th.clone(), init_al.clone(), init_be.clone()
-    cfg = M.FitConfig(max_iters=args.iters, optimizer="adam", lr=0.05, tol_rel=0.0)
+    cfg = M.FitConfig(max_iters=args.iters, optimizer="adam", lr=0.05, tol_rel=args.tol, patience=10)
     from paper_2411_10258_b200 import shard
     rec = torch.empty(W, shard.record_width(D), dtype=torch.float32, device=dev)
     gathered = [torch.empty_like(rec) for _ in range(world)] if (world > 1 and rank == 0) else None
@@ -531,7 +534,10 @@ def main():
             "data": f"synthetic (Ogata-thinned MDHP on GPU, recipe {rname}, seed {args.seed}"
                     + (f", {args.inject} injections in attack windows" if args.inject != "none" else "") + ")",
             "config": {"workload": f"{args.config}: {W} windows/GPU, D={D}, ~{E // max(W, 1)} events/window, "
-                                   f"T={rc.T}s, Adam lr 0.05, {args.iters} fixed iterations + final eval",
+                                   f"T={rc.T}s, Adam lr 0.05, "
+                                   + (f"{args.iters} fixed iterations + final eval" if args.tol <= 0 else
+                                      f"converged mode: tol_rel {args.tol:g}, patience 10, at most {args.iters} "
+                                      f"iterations (mean {float(iters_run.double().mean()):.1f}) + final eval"),
                        "windows_per_gpu": W, "events_per_gpu": E, "D": D, "iterations": args.iters,
                        "l2": "inputs larger than L2 (packed events ~%.1f GB/GPU vs 126 MB L2)" % (E * 9 / 1e9),
                        "parallelism": f"windows sharded over {world} GPU(s), final NCCL gather"},
