@@ -118,3 +118,30 @@ def test_cfg1_500_gd():
         got = got.cpu().numpy()
         assert np.all(np.abs(got - ref) <= 1e-3 * np.maximum(np.abs(ref), 1e-2 * np.mean(np.abs(ref)))), (got, ref)
     np.testing.assert_allclose(fr["trace"][0].cpu().numpy(), o["trace"], rtol=1e-4)
+
+
+def test_cfg5_full_bench_fit_500():
+    """The bench step itself: 1,048,576 cfg5 windows, SPEC init, Adam lr 0.05, 500 fixed
+    iterations in one persistent mdhp_fit launch; the fitted lnL of sampled windows (first,
+    last, 6 random) equals the fp64 oracle's 500-iteration fit within 1e-4 relative (R18: long
+    Adam runs are compared through lnL)."""
+    W, D = 1 << 20, 16
+    b = sg.make_batch_gpu("cfg5", W, seed=2024)
+    pk = M.pack_windows(D, b["t"], b["mark"], b["win_off"], b["T"], time_mode=1)
+    th0 = torch.full((W, D), 0.1, device=DEV); al0 = torch.full((W, D, D), 0.5, device=DEV)
+    be0 = torch.full((W, D, D), 1.0, device=DEV)
+    kw = dict(max_iters=500, optimizer="adam", lr=0.05, tol_rel=0.0)
+    th, al, be = th0.clone(), al0.clone(), be0.clone()
+    fr = M.fit(pk, th, al, be, M.FitConfig(**kw))
+    torch.cuda.synchronize()
+    assert np.all(fr["iters"].cpu().numpy() == 500)
+    lnl = fr["lnl"].cpu().numpy()
+    assert np.all(np.isfinite(lnl))
+    rng = np.random.default_rng(11)
+    for w in sorted({0, W - 1} | set(rng.choice(W, 6, replace=False).tolist())):
+        t, m = _host(b, w)
+        t32, T32, st = oracle.convert_window(D, t, m, float(b["T"][w]), 1, tie_policy=oracle.TIE_NUDGE)
+        o = oracle.fit(D, t32, m, T32, np.full(D, 0.1), np.full((D, D), 0.5), np.full((D, D), 1.0),
+                       oracle.FitConfig(**kw))
+        assert o["iters"] == 500
+        assert abs(lnl[w] - o["lnl"]) <= 1e-4 * abs(o["lnl"]), (w, lnl[w], o["lnl"])
