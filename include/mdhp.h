@@ -173,6 +173,10 @@ typedef struct {
     float    min_param;     /* projection floor for theta and beta; alpha floor is 0 */
     uint32_t fit_mask;      /* MDHP_FIT_* groups that are updated; others keep their init   */
     int32_t  max_halvings;  /* non-finite evaluation: roll back, halve lr           */
+    int32_t  adam_step0;    /* Adam steps already taken (bias-correction offset) when resuming
+                               from a returned opt_state; 0 for a fresh fit.  fit(k) then
+                               fit(m, opt_state, adam_step0 = k) == fit(k + m) in fixed-
+                               iteration mode (checkpoint / resume)        */
 } mdhp_fit_config;
 
 /*
@@ -182,7 +186,8 @@ typedef struct {
  *
  *   theta, alpha, beta  in: initial parameters; out: fitted (projected) parameters
  *   opt_state [W][2][D + 2 D^2] fp32 Adam moments (m then v, each in theta|alpha|beta order),
- *             in/out; NULL -> zero-initialised internal workspace (resume = pass it back)
+ *             in/out; NULL -> zero-initialised internal workspace (resume = pass it back
+ *             with cfg->adam_step0 = the iterations already run)
  *   loglik [W]   fp64 out: lnL at the returned parameters
  *   iters  [W]   int32 out: iterations run
  *   win_status [W] in: from mdhp_pack_windows; out: OR-ed with NONFINITE / DIVERGED / CONVERGED

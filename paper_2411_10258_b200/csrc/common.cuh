@@ -139,7 +139,7 @@ __device__ __forceinline__ int group_max_i(int v) {
 }
 
 struct FitCfgDev {
-  int max_iters, optimizer, loss_mean, patience, max_halvings;
+  int max_iters, optimizer, loss_mean, patience, max_halvings, step0;
   float lr, b1, b2, eps, tol_rel, min_param;
   unsigned fit_mask;
 };

@@ -233,7 +233,7 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
     const int n = live ? P.n[w] : 0;
     const float scale = (cfg.loss_mean && n > 0) ? 1.0f / (float)n : 1.0f;
     // per-window (group-uniform) optimizer state
-    int it = 0, s = 0, halv = 0, stall = 0, st = 0;
+    int it = 0, s = cfg.step0, halv = 0, stall = 0, st = 0;   // s: Adam step (resume offset)
     float lr_w = cfg.lr;
     double lnl_prev = 0.0;
     bool have_prev = false, have_lnl = false;

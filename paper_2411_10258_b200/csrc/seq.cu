@@ -955,6 +955,7 @@ int seq_fit_launch(int D, int64_t N, int ce, double T, const void* pk, const Fit
   // control block: done = (invalid input or max_iters == 0), lr_w = lr
   SeqCtl h{};
   h.lr_w = cfg.lr;
+  h.s = cfg.step0;   // Adam bias-correction offset when resuming
   h.done = cfg.max_iters <= 0;
   cudaMemcpyAsync(w.ctl, &h, sizeof(SeqCtl), cudaMemcpyHostToDevice, st);
   // an invalid sequence (validation bits) is not fitted
@@ -1128,6 +1129,7 @@ int seq_slice_init_launch(int D, int64_t N, int ce, void* work, const FitCfgDev*
     SeqWork w = slice_work(D, N, ce, work);
     SeqCtl h{};
     h.lr_w = cfg->lr;
+    h.s = cfg->step0;
     h.done = cfg->max_iters <= 0;
     if (cudaMemcpyAsync(w.ctl, &h, sizeof(SeqCtl), cudaMemcpyHostToDevice, st) != cudaSuccess)
       return MDHP_ECUDA;

@@ -291,3 +291,34 @@ def test_fit_host_end_to_end():
     np.testing.assert_array_equal(th.numpy(), th_d.cpu().numpy())
     np.testing.assert_array_equal(be.numpy(), be_d.cpu().numpy())
     np.testing.assert_array_equal(r["lnl"].numpy(), rd["lnl"].cpu().numpy())
+
+
+def test_fit_resume_is_exact():
+    """Checkpoint / resume: fit(120) then fit(80) from the returned
+    parameters and Adam moments with adam_step0 = 120 equals one fit(200) bit for bit."""
+    D = 16
+    b, _ = H.small_batch(D, 9, seed=77, edges=False)
+    W = len(b["T"])
+    pk = M.pack_windows(D, *dev_batch(b))
+    P = D + 2 * D * D
+    init = (torch.full((W, D), 0.1, device=DEV), torch.full((W, D, D), 0.5, device=DEV),
+            torch.full((W, D, D), 1.0, device=DEV))
+    kw = dict(optimizer="adam", lr=0.05, tol_rel=0.0)
+    a = [x.clone() for x in init]
+    opt_a = torch.zeros(W, 2 * P, device=DEV)
+    ra = M.fit(pk, *a, M.FitConfig(max_iters=200, **kw), opt_state=opt_a)
+    c = [x.clone() for x in init]
+    opt_c = torch.zeros(W, 2 * P, device=DEV)
+    M.fit(pk, *c, M.FitConfig(max_iters=120, **kw), opt_state=opt_c)
+    rc = M.fit(pk, *c, M.FitConfig(max_iters=80, adam_step0=120, **kw), opt_state=opt_c)
+    torch.cuda.synchronize()
+    for x, y in zip(a, c):
+        assert torch.equal(x, y)
+    assert torch.equal(opt_a, opt_c) and torch.equal(ra["lnl"], rc["lnl"])
+    # without the step offset the bias correction restarts: not the same trajectory
+    d = [x.clone() for x in init]
+    opt_d = torch.zeros(W, 2 * P, device=DEV)
+    M.fit(pk, *d, M.FitConfig(max_iters=120, **kw), opt_state=opt_d)
+    M.fit(pk, *d, M.FitConfig(max_iters=80, **kw), opt_state=opt_d)
+    torch.cuda.synchronize()
+    assert not torch.equal(a[2], d[2])

@@ -136,3 +136,26 @@ def test_seq_cfg4_full_size():
     th, al, be = (b[k][0].cpu().numpy() for k in ("theta", "alpha", "beta"))
     out, ref, rel = check(D, t, m, 1000.0, th, al, be, ce=256, what="cfg4", use_def=False)
     assert rel < 1e-5
+
+
+def test_seq_fit_resume_is_exact():
+    """Long-sequence fit: fit(15) + fit(10, opt_state, adam_step0=15) == fit(25) bit for bit."""
+    D = 3
+    t, m, _ = seq_case(D, 30.0, 30.0, seed=32)
+    ps = M.seq_pack(D, torch.tensor(t, device=DEV), torch.tensor(m, dtype=torch.int32, device=DEV), 30.0,
+                    chunk_events=32)
+    P = D + 2 * D * D
+    init = (torch.full((D,), 2.0, device=DEV), torch.full((D, D), 0.5, device=DEV),
+            torch.full((D, D), 2.0, device=DEV))
+    kw = dict(optimizer="adam", lr=0.05, tol_rel=0.0)
+    a = [x.clone() for x in init]
+    oa = torch.zeros(2 * P, device=DEV)
+    ra = M.seq_fit(ps, *a, M.FitConfig(max_iters=25, **kw), opt_state=oa)
+    c = [x.clone() for x in init]
+    oc = torch.zeros(2 * P, device=DEV)
+    M.seq_fit(ps, *c, M.FitConfig(max_iters=15, **kw), opt_state=oc)
+    rc = M.seq_fit(ps, *c, M.FitConfig(max_iters=10, adam_step0=15, **kw), opt_state=oc)
+    torch.cuda.synchronize()
+    for x, y in zip(a, c):
+        assert torch.equal(x, y)
+    assert torch.equal(oa, oc) and torch.equal(ra["lnl"], rc["lnl"])
