@@ -306,7 +306,18 @@ def cpu_baseline(b_host, D, rc, iters, n_windows, seed):
     ev_it = float(np.sum(np.diff(off) * evals))
     return {"value": ev_it / dt, "unit": UNIT, "cores": ncores, "kind": "oracle",
             "sample": f"{W} windows of the same workload x {iters} Adam iterations (+1 final evaluation), "
-                      f"fp64 eager recursion, {dt:.1f} s wall", "windows_per_s": W / dt}
+                      f"fp64 eager recursion, {dt:.1f} s wall", "windows_per_s": W / dt,
+            "cpu_model": cpu_model()}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def reference_arm(args):
