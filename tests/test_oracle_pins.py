@@ -424,3 +424,27 @@ def test_batch_equals_single():
         a, z = b["win_off"][w], b["win_off"][w + 1]
         r = oracle.fit(D, t32[a:z], b["mark"][a:z], 1.0, th[w], al[w], be[w], cfg)
         assert fb["lnl"][w] == r["lnl"] and np.array_equal(fb["alpha"][w], r["alpha"])
+
+
+def test_mark_relabeling_invariance():
+    """Relabelling the marks by a permutation pi (and theta, alpha, beta with it:
+    theta'[pi i] = theta[i], alpha'[pi i][pi j] = alpha[i][j]) leaves lnL unchanged and permutes
+    the gradients the same way.  Catches any index that mixes target and source (alpha[i][j]
+    used as alpha[j][i]) on non-symmetric parameters, in both routes."""
+    rng = np.random.default_rng(21)
+    for k in range(12):
+        D = int(rng.integers(2, 6))
+        t, m, T, th, al, be = _rand_case(rng, D, 8, T=1.3, ties=(k % 2 == 0))
+        pi = rng.permutation(D)
+        inv = np.argsort(pi)
+        m2 = pi[m].astype(np.int32)
+        th2 = th[inv]
+        al2 = al[np.ix_(inv, inv)]
+        be2 = be[np.ix_(inv, inv)]
+        for fn in (oracle.loglik_def, oracle.loglik_rec):
+            a = fn(D, t, m, T, th, al, be)
+            b = fn(D, t, m2, T, th2, al2, be2)
+            assert b["lnl"] == pytest.approx(a["lnl"], rel=1e-13, abs=1e-13)
+            np.testing.assert_allclose(b["g_theta"], a["g_theta"][inv], rtol=1e-12, atol=1e-12)
+            np.testing.assert_allclose(b["g_alpha"], a["g_alpha"][np.ix_(inv, inv)], rtol=1e-12, atol=1e-12)
+            np.testing.assert_allclose(b["g_beta"], a["g_beta"][np.ix_(inv, inv)], rtol=1e-11, atol=1e-11)
