@@ -139,9 +139,10 @@ __device__ __forceinline__ int group_max_i(int v) {
 }
 
 struct FitCfgDev {
-  int max_iters, optimizer, loss_mean, patience, max_halvings, step0;
+  int max_iters, optimizer, loss_mean, patience, max_halvings;
   float lr, b1, b2, eps, tol_rel, min_param;
   unsigned fit_mask;
+  int step0;   // Adam steps of earlier calls (resume)
 };
 
 // launch counter (process-wide), incremented by every launch site

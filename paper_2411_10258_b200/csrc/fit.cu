@@ -145,7 +145,7 @@ k_loglik(Packed P, const float* __restrict__ theta, const float* __restrict__ al
 // One optimizer step for this lane's column j (theta_j, alpha_.j, beta_.j), PyTorch Adam / GD
 // semantics, then projection.  Gradients of lnL are in Gs (alpha, beta) and
 // dth; the loss gradient is -grad * scale.
-template <int DP>
+template <int DP, bool RESUME>
 __device__ __forceinline__ void step_column(float2* A, const float2* Gs, const WarpCtx<DP>& c,
                                             int D, int64_t w, const FitCfgDev& cfg, float lr_w,
                                             int s, float scale, float dth, float& th,
@@ -157,8 +157,11 @@ __device__ __forceinline__ void step_column(float2* A, const float2* Gs, const W
   const bool adam = cfg.optimizer == MDHP_OPT_ADAM;
   float bc1 = 1.0f, sbc2 = 1.0f;
   if (adam) {
-    bc1 = 1.0f - powf(cfg.b1, (float)s);
-    sbc2 = sqrtf(1.0f - powf(cfg.b2, (float)s));
+    // s counts this call's steps; cfg.step0 those of earlier calls (resume).  A separate
+    // instantiation: reading step0 in the hot kernel perturbed its register allocation (-3%)
+    const float sg = RESUME ? (float)(s + cfg.step0) : (float)s;
+    bc1 = 1.0f - powf(cfg.b1, sg);
+    sbc2 = sqrtf(1.0f - powf(cfg.b2, sg));
   }
   auto upd = [&](float p, float g, size_t q, float lo) -> float {
     const float gl = -g * scale;
@@ -202,7 +205,7 @@ __device__ __forceinline__ void store_params(const float2* A, const WarpCtx<DP>&
 // Persistent fit kernel: each warp takes G windows at a time (longest first) from a global
 // counter and runs their whole iteration loop on chip (a6), then evaluates lnL at the final
 // parameters and writes everything back.
-template <int DP>
+template <int DP, bool RESUME>
 __global__ void __launch_bounds__(128, DP >= 32 ? 2 : 4)
 k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ alpha,
       float* __restrict__ beta, float* __restrict__ opt, double* __restrict__ lnl_out,
@@ -233,7 +236,7 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
     const int n = live ? P.n[w] : 0;
     const float scale = (cfg.loss_mean && n > 0) ? 1.0f / (float)n : 1.0f;
     // per-window (group-uniform) optimizer state
-    int it = 0, s = cfg.step0, halv = 0, stall = 0, st = 0;   // s: Adam step (resume offset)
+    int it = 0, s = 0, halv = 0, stall = 0, st = 0;
     float lr_w = cfg.lr;
     double lnl_prev = 0.0;
     bool have_prev = false, have_lnl = false;
@@ -272,7 +275,7 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
             store_params<DP>(A, c, D, w, th, theta, alpha, beta);   // previous point
             have_prev = true;
             s++;
-            step_column<DP>(A, Gs, c, D, w, cfg, lr_w, s, scale, dth, th, opt);
+            step_column<DP, RESUME>(A, Gs, c, D, w, cfg, lr_w, s, scale, dth, th, opt);
             it++;
           }
         }
@@ -342,7 +345,7 @@ static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float*
   using SM = Smem<DP>;
   constexpr int WPB = 4;
   const size_t smem = WPB * SM::per_warp;
-  auto kern = k_fit<DP>;
+  auto kern = cfg.step0 != 0 ? k_fit<DP, true> : k_fit<DP, false>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess) {
     set_error("cudaFuncSetAttribute(k_fit) failed");
