@@ -11,8 +11,9 @@ LIB = os.path.join(LIBDIR, "libmdhp.so")
 LIB_DEBUG = os.path.join(LIBDIR, "libmdhp_debug.so")   # -DMDHP_DEBUG: device bounds asserts
 SOURCES = ["abi.cu", "pack.cu", "fit.cu", "seq.cu", "dense.cu", "features.cu"]
 HEADERS = ["common.cuh", "eval.cuh"]
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xlinker", "--no-undefined"]
+CC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+            "-Xcompiler", "-fPIC"]
+LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xlinker", "--no-undefined"]
 
 
 def _stale(out, deps):
@@ -29,14 +30,28 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     os.makedirs(LIBDIR, exist_ok=True)
     out = LIB_DEBUG if debug else LIB
     if force or _stale(out, deps):
-        cmd = ["nvcc", *NVCC_FLAGS, *(["-DMDHP_DEBUG"] if debug else []), "-o", out, *srcs]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
+        # one object per source, compiled in parallel, then one link
+        from concurrent.futures import ThreadPoolExecutor
+        objdir = os.path.join(LIBDIR, "obj")
+        os.makedirs(objdir, exist_ok=True)
+        tag = ".dbg" if debug else ""
+        objs = [os.path.join(objdir, os.path.basename(s)[:-3] + tag + ".o") for s in srcs]
+
+        def cc(src, obj):
+            cmd = ["nvcc", *CC_FLAGS, *(["-DMDHP_DEBUG"] if debug else []),
+                   *(["-Xptxas=-v"] if verbose else []), "-c", "-o", obj, src]
+            return cmd, subprocess.run(cmd, capture_output=True, text=True)
+
+        with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
+            for cmd, r in ex.map(lambda a: cc(*a), zip(srcs, objs)):
+                if r.returncode != 0:
+                    raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+                if verbose:
+                    print(r.stderr)
+        cmd = ["nvcc", *LINK_FLAGS, "-o", out, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
-            raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
-        if verbose:
-            print(r.stderr)
+            raise RuntimeError("nvcc link failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
     return out
 
 
