@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--inject", default="none", choices=["none", "PLA", "DEA", "ASA", "DAM"],
                     help="time-exciting injections (Table II + Algorithm 4) in attack windows (row f2)")
+    ap.add_argument("--loglik", action="store_true",
+                    help="time mdhp_loglik_grad alone (rows a2-a5, SURVEY 8(d)) on the config's windows")
     ap.add_argument("--tol", type=float, default=0.0,
                     help="converged mode (SURVEY 8(d)): tol_rel (e.g. 1e-6, patience 10, capped at --iters); "
                          "0 = fixed-iteration mode (the headline)")
@@ -64,6 +66,42 @@ WORKLOADS = {
     "cfg5": ("cfg5", 1 << 20),
     "feat": ("cfg5", 1 << 20),   # row f4: Hawkes-gate features of cfg5-sized fitted parameters
 }
+
+
+def bench_loglik(args, rc, b, W, world, rank, dev):
+    """--loglik: one mdhp_loglik_grad call (lnL + gradient of every window, rows a2-a5) per step
+    at the fitted-like truth parameters; events per second of kernel time."""
+    import torch
+    import paper_2411_10258_b200 as M
+    D = rc.D
+    E = int(b["win_off"][-1])
+    pk = M.pack_windows(D, b["t"], b["mark"], b["win_off"], b["T"], time_mode=1)
+    th, al, be = b["theta"], b["alpha"], b["beta"]
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        M.loglik_grad(pk, th, al, be)
+    torch.cuda.synchronize()
+    L0 = M.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        M.loglik_grad(pk, th, al, be)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    Dp = 1 << (D - 1).bit_length()
+    mufu = E * (2 * D + 2) / (ms / 1e3) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": "mdhp_loglik_grad events/s (lnL + gradient, rows a2-a5)", "value": E / (ms / 1e3),
+            "unit": "events/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": f"synthetic (recipe {args.config}, seed {args.seed}), truth parameters",
+            "config": {"workload": f"{args.config}: {W} windows, D={D}, {E} events, one evaluation per step"},
+            "roofline": {"bound": "alu", "achieved": mufu, "peak": MUFU_PEAK_GOPS, "unit": "Gop/s (MUFU)",
+                         "frac": mufu / MUFU_PEAK_GOPS, "traffic": None, "kernel": f"k_loglik<{Dp}>"},
+            "gpu_launches": int(M.launch_count() - L0)}), flush=True)
+    return 0
 
 
 def bench_features(args, world, rank, dev):
@@ -403,6 +441,8 @@ def main():
         return bench_features(args, world, rank, dev)
     first, _ = (rank * W, W)
     b = sgpu.make_batch_gpu(rc, W, seed=args.seed, first_window=first, device=dev)
+    if args.loglik:
+        return bench_loglik(args, rc, b, W, world, rank, dev)
     E = int(b["win_off"][-1])
     init_th = torch.full((W, D), 0.1, device=dev)
     init_al = torch.full((W, D, D), 0.5, device=dev)
