@@ -47,7 +47,7 @@ def invalid_windows(D):
     return w
 
 
-@pytest.mark.parametrize("D", [1, 2, 3, 5, 8, 16, 32])
+@pytest.mark.parametrize("D", [1, 2, 3, 5, 8, 12, 16, 20, 32])
 def test_pack_parity(D):
     """Packed fp32 times, marks, per-mark gaps and counts bit-exact; status words equal to the
     oracle's packing definition; the order is a longest-first permutation."""
@@ -110,7 +110,7 @@ def _check_loglik(D, b, th, al, be, what, time_mode=mdhp.TIME_RAW, use_def=True)
     return worst
 
 
-@pytest.mark.parametrize("D", [1, 2, 3, 5, 8, 16, 32])
+@pytest.mark.parametrize("D", [1, 2, 3, 5, 8, 12, 16, 20, 32])
 def test_loglik_parity_truth_and_random(D):
     """lnL and gradients at the generating parameters and at random parameters (ties, empty
     dims, events at 0 and T included via edge windows; several windows per warp; ragged)."""
@@ -202,7 +202,7 @@ def _param_close(got, ref, floor_frac=1e-2, rel=1e-3, what=""):
     assert not bad.any(), f"{what}: {np.argwhere(bad)[:4].tolist()} got {got[bad][:4]} ref {ref[bad][:4]}"
 
 
-@pytest.mark.parametrize("D", [2, 5, 8, 16])
+@pytest.mark.parametrize("D", [2, 5, 8, 12, 16, 20])
 def test_fit_gd_fixed_iters(D):
     """GD on the mean loss, fixed iteration count: fitted parameters within 1e-3 relative."""
     b, (th, al, be) = H.small_batch(D, 10, seed=200 + D, edges=False)

@@ -56,7 +56,7 @@ def check(D, t, m, T, th, al, be, ce, what, use_def=True):
     return out, ref, rel
 
 
-@pytest.mark.parametrize("D", [1, 3, 8, 16])
+@pytest.mark.parametrize("D", [1, 3, 8, 12, 16, 20])
 def test_seq_vs_definition(D):
     """Several hundred chunks; lnL within 1e-4 (expected ~1e-6) of Eq.(5) written out."""
     t, m, p = seq_case(D, 60.0, 40.0, seed=10 + D)
