@@ -322,3 +322,31 @@ def test_fit_resume_is_exact():
     M.fit(pk, *d, M.FitConfig(max_iters=80, **kw), opt_state=opt_d)
     torch.cuda.synchronize()
     assert not torch.equal(a[2], d[2])
+
+
+def test_very_long_window_among_short_ones():
+    """One 60,000-event window (Poisson, D = 8) in a batch of short and empty windows: the
+    longest-first schedule, 32-bit per-window offsets and the null-chunk padding of the short
+    windows sharing its warps; lnL and gradients vs the oracle."""
+    D = 8
+    rng = np.random.default_rng(5)
+    long_t, long_m = gen.poisson_window(np.full(D, 6000.0), 1.0, rng)
+    assert len(long_t) > 40000
+    short, _ = H.small_batch(D, 6, seed=8, edges=True)
+    wins = [(long_t, long_m)] + [(short["t"][short["win_off"][w]:short["win_off"][w + 1]],
+                                  short["mark"][short["win_off"][w]:short["win_off"][w + 1]])
+                                 for w in range(len(short["T"]))]
+    b = H.batch_from_windows(wins, 1.0)
+    W = len(b["T"])
+    th, al, be = H.random_params(rng, W, D, scale_theta=(100.0, 3000.0), alpha=(0.0, 20.0),
+                                 beta=(5.0, 200.0))
+    got, _ = gpu_loglik(D, b, th, al, be)
+    t32, T32, st = H.oracle_times(b, D)
+    for w in range(W):
+        a, z = b["win_off"][w], b["win_off"][w + 1]
+        ref = oracle.loglik_rec(D, t32[a:z], b["mark"][a:z], T32[w], th[w], al[w], be[w])
+        assert abs(got["lnl"][w] - ref["lnl"]) <= 1e-4 * abs(ref["lnl"]), (w, got["lnl"][w], ref["lnl"])
+        sth, sal, sbe = H.grad_scales(t32[a:z], b["mark"][a:z], T32[w], th[w], al[w], be[w], ref)
+        H.assert_grad_close(got["g_theta"][w], ref["g_theta"], sth, what=f"w{w} theta")
+        H.assert_grad_close(got["g_alpha"][w], ref["g_alpha"], sal, what=f"w{w} alpha")
+        H.assert_grad_close(got["g_beta"][w], ref["g_beta"], sbe, what=f"w{w} beta")
