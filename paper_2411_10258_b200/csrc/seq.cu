@@ -599,7 +599,18 @@ __global__ void k_seq_gate(const int32_t* __restrict__ pst, int* __restrict__ ct
 }
 
 // Phase 4b: epilogue (+ optional optimizer step for the sequence fit).  One block of D^2
-// threads (thread = pair (i, j), target-major).
+// threads (thread = pair (i, j), target-major), rounded up to whole warps.
+__device__ __forceinline__ double block_sum_d(double v, double* red) {
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int k = 0; k < (int)(blockDim.x >> 5); k++) s += red[k];   // fixed order: deterministic
+  __syncthreads();
+  return s;
+}
+inline unsigned finish_threads(int D) { return (unsigned)(((D * D + 31) / 32) * 32); }
+
 __global__ void __launch_bounds__(1024)
 k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
              const int32_t* __restrict__ cnt, const float* __restrict__ umax,
@@ -616,7 +627,7 @@ k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
   const bool invalid = (pstatus[0] & MDHP_ST_INVALID) != 0;
   SeqCtl* ctl = reinterpret_cast<SeqCtl*>(ctl_i);
   if (ctl && ctl->done && grad) return;
-  __shared__ double red[1024];
+  __shared__ double red[32];
   __shared__ int okflag;
   const int tid = threadIdx.x;
   const int DD = D * D;
@@ -653,21 +664,8 @@ k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
     dth = gthv[tid] - (float)T;
     if (!isfinite(dth)) okflag = 0;
   }
-  red[tid] = part3;
-  __syncthreads();
-  for (int o = 512; o >= 1; o >>= 1) {
-    if (tid < o) red[tid] += red[tid + o];
-    __syncthreads();
-  }
-  const double p3 = red[0];
-  __syncthreads();
-  red[tid] = sth;
-  __syncthreads();
-  for (int o = 512; o >= 1; o >>= 1) {
-    if (tid < o) red[tid] += red[tid + o];
-    __syncthreads();
-  }
-  const double lnl = (double)kLn2 * ls[0] + p3 - T * red[0];
+  const double p3 = block_sum_d(part3, red);
+  const double lnl = (double)kLn2 * ls[0] + p3 - T * block_sum_d(sth, red);
   if (!ctl) {
     if (tid == 0) lnl_out[0] = invalid ? (double)NAN : lnl;
     if (grad) {
@@ -930,7 +928,7 @@ int seq_loglik_launch(int D, int64_t N, int ce, double T, const void* pk, const 
   seq_phases(L, pk, th, al, be, w, grad, nullptr, st);
   seq_reduce(L, w, grad, nullptr, st);
   FitCfgDev cfg{};
-  k_seq_finish<<<1, 1024, 0, st>>>(D, L.Dp, T, at<float>(pk, L.tail), at<int32_t>(pk, L.cnt),
+  k_seq_finish<<<1, finish_threads(D), 0, st>>>(D, L.Dp, T, at<float>(pk, L.tail), at<int32_t>(pk, L.cnt),
                                    at<float>(pk, L.umax), at<float>(pk, L.mom), w.fin, w.gsum,
                                    w.gth, w.ls, const_cast<float*>(th), const_cast<float*>(al),
                                    const_cast<float*>(be), lnl, gt, ga, gb, grad, nullptr, cfg,
@@ -968,7 +966,7 @@ int seq_fit_launch(int D, int64_t N, int ce, double T, const void* pk, const Fit
   auto iteration = [&](cudaStream_t s) {
     seq_phases(L, pk, th, al, be, w, 1, w.ctl, s);
     seq_reduce(L, w, 1, w.ctl, s);
-    k_seq_finish<<<1, 1024, 0, s>>>(D, L.Dp, T, at<float>(pk, L.tail), at<int32_t>(pk, L.cnt),
+    k_seq_finish<<<1, finish_threads(D), 0, s>>>(D, L.Dp, T, at<float>(pk, L.tail), at<int32_t>(pk, L.cnt),
                                     at<float>(pk, L.umax), at<float>(pk, L.mom), w.fin, w.gsum,
                                     w.gth, w.ls, th, al, be, lnl, nullptr, nullptr, nullptr, 1,
                                     w.ctl, cfg, w.prev, opt, trace, N, status, iters,
@@ -1008,7 +1006,7 @@ int seq_fit_launch(int D, int64_t N, int ce, double T, const void* pk, const Fit
   // lnL at the returned point
   seq_phases(L, pk, th, al, be, w, 0, nullptr, st);
   seq_reduce(L, w, 0, nullptr, st);
-  k_seq_finish<<<1, 1024, 0, st>>>(D, L.Dp, T, at<float>(pk, L.tail), at<int32_t>(pk, L.cnt),
+  k_seq_finish<<<1, finish_threads(D), 0, st>>>(D, L.Dp, T, at<float>(pk, L.tail), at<int32_t>(pk, L.cnt),
                                    at<float>(pk, L.umax), at<float>(pk, L.mom), w.fin, w.gsum,
                                    w.gth, w.ls, th, al, be, lnl, nullptr, nullptr, nullptr, 0,
                                    w.ctl, cfg, w.prev, opt, trace, N, status, iters,
@@ -1212,7 +1210,7 @@ int seq_finish_launch(int D, int64_t N_total, int ce, int64_t N_slice, double T,
   FitCfgDev c0{};
   const FitCfgDev& c = cfg ? *cfg : c0;
   const int grad = cfg ? (final_eval ? 0 : 1) : (gt != nullptr);
-  k_seq_finish<<<1, 1024, 0, st>>>(D, L.Dp, T, a.tail, a.cnt, a.umax, a.mom, fin, a.gsum, a.gth,
+  k_seq_finish<<<1, finish_threads(D), 0, st>>>(D, L.Dp, T, a.tail, a.cnt, a.umax, a.mom, fin, a.gsum, a.gth,
                                    a.ls, th, al, be, lnl, gt, ga, gb, grad,
                                    cfg ? w.ctl : nullptr, c, w.prev, opt ? opt : w.opt, trace,
                                    N_total, status, iters, pstatus);
