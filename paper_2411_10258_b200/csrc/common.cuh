@@ -119,6 +119,19 @@ __device__ __forceinline__ float rcpf(float x) {
   return y;
 }
 
+// Asynchronous global -> shared copies (cp.async, L1-allocating): a prologue that stages many
+// small loads pays one round trip at the final wait instead of one per dependent store.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc) {
+  static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16, "cp.async size");
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(gsrc), "n"(BYTES)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 template <int DP>
 __device__ __forceinline__ float group_sum(float v) {
 #pragma unroll

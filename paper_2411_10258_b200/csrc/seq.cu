@@ -325,8 +325,11 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
   const int n = live ? (int)(cstart[c + 1] - cstart[c]) : 0;
   for (int i = 0; i < DP; i++) {
     SQ[j * RS + i] = make_float2(0.0f, 0.0f);
-    B[j * RS + i] = (j < D && i < D) ? beta[(size_t)j * D + i] : 0.0f;   // beta_ji: row j, col i
+    // beta_ji: row j, col i
+    if (j < D && i < D) cp_async<4>(&B[j * RS + i], beta + (size_t)j * D + i);
+    else B[j * RS + i] = 0.0f;
   }
+  cp_async_wait_all();
   // column DP: the null event's (never read) column
   SQ[j * RS + DP] = make_float2(0.0f, 0.0f);
   B[j * RS + DP] = 0.0f;
@@ -399,7 +402,12 @@ __device__ __forceinline__ AffMap compose(const AffMap& m1, const AffMap& m2) {
   return r;
 }
 
-constexpr int kScanP = 4, kScanS = 256;   // pairs x segments per scan block (1024 threads)
+#ifndef MDHP_SCAN_P
+#define MDHP_SCAN_P 4
+#endif
+constexpr int kScanP = MDHP_SCAN_P, kScanS = 1024 / MDHP_SCAN_P;   // pairs x segments per scan
+                                                                  // block (1024 threads)
+constexpr int kScanB = 4;                  // chunks per load batch of a segment walk
 
 __global__ void __launch_bounds__(kScanP * kScanS)
 k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __restrict__ beta,
@@ -416,13 +424,26 @@ k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __res
   const float b = valid ? beta[p] : 0.0f;
   const int64_t per = (C + kScanS - 1) / kScanS;
   const int64_t c0 = min(C, (int64_t)seg * per), c1 = min(C, c0 + per);
+  // segment walks in batches of kScanB chunks: all loads of a batch are issued before the
+  // (sequential) compose chain uses them, instead of one L2 round trip per chunk
   AffMap m{1.0f, 0.0f, 0.0f, 0.0f};
   if (valid) {
-    for (int64_t c = c0; c < c1; c++) {
-      const float L = cspan[c];
-      const float2 l = loc[c * DD + p];
-      const AffMap mc{ex2f(b * (L * -kLog2e)), L, l.x, l.y};
-      m = compose(m, mc);
+    for (int64_t c = c0; c < c1; c += kScanB) {
+      float Lb[kScanB];
+      float2 lb[kScanB];
+#pragma unroll
+      for (int k = 0; k < kScanB; k++) {
+        const bool in = c + k < c1;
+        Lb[k] = in ? cspan[c + k] : 0.0f;
+        lb[k] = in ? loc[(c + k) * DD + p] : make_float2(0.0f, 0.0f);
+      }
+#pragma unroll
+      for (int k = 0; k < kScanB; k++) {
+        if (c + k < c1) {
+          const AffMap mc{ex2f(b * (Lb[k] * -kLog2e)), Lb[k], lb[k].x, lb[k].y};
+          m = compose(m, mc);
+        }
+      }
     }
   }
   sm[seg][lane] = m;
@@ -457,18 +478,29 @@ k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __res
   if (maps_only) return;
   // state entering segment seg = (inclusive map of segment seg-1) applied to the carried state
   float2 x = seg > 0 ? apply(sm[seg - 1][lane], x0) : x0;
-  for (int64_t c = c0; c < c1; c++) {
-    carry[c * DD + p] = x;
-    const float L = cspan[c];
-    const float2 l = loc[c * DD + p];
-    const float e = ex2f(b * (L * -kLog2e));
-    x = make_float2(fmaf(e, x.x, l.x), fmaf(e, fmaf(L, x.x, x.y), l.y));
+  for (int64_t c = c0; c < c1; c += kScanB) {
+    float Lb[kScanB];
+    float2 lb[kScanB];
+#pragma unroll
+    for (int k = 0; k < kScanB; k++) {
+      const bool in = c + k < c1;
+      Lb[k] = in ? cspan[c + k] : 0.0f;
+      lb[k] = in ? loc[(c + k) * DD + p] : make_float2(0.0f, 0.0f);
+    }
+#pragma unroll
+    for (int k = 0; k < kScanB; k++) {
+      if (c + k < c1) {
+        carry[(c + k) * DD + p] = x;
+        const float e = ex2f(b * (Lb[k] * -kLog2e));
+        x = make_float2(fmaf(e, x.x, lb[k].x), fmaf(e, fmaf(Lb[k], x.x, x.y), lb[k].y));
+      }
+    }
   }
 }
 
 // Phase 3: full event loop per chunk from its carried-in state; per-chunk partial sums.
 template <int DP>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 4)
 k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* __restrict__ cbeg,
            const float* __restrict__ t32, const float* __restrict__ dtp,
            const uint8_t* __restrict__ mk, const float* __restrict__ theta,
@@ -488,13 +520,24 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
   const int64_t c = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wid) * SM::G + g;
   const bool live = c < C;
   const size_t DD = (size_t)D * D;
+  // parameters and the carried-in state go straight to shared memory with cp.async (one round
+  // trip at the wait below instead of one per row: this prologue was ~15% of the kernel)
   for (int i = 0; i < DP; i++) {
     const bool real = live && i < D && j < D;
-    A[i * RS + j] = real ? ab_pack<DP>(i, alpha[(size_t)i * D + j], beta[(size_t)i * D + j])
-                         : ab_pack<DP>(i, 0.0f, 1.0f);
-    SQ[i * RS + j] = real ? carry[(size_t)c * DD + (size_t)i * D + j] : make_float2(0.0f, 0.0f);
+    float2* a = &A[i * RS + j];
+    if (real) {
+      float* af = reinterpret_cast<float*>(a);
+      const bool sw = ab_swapped<DP>(i);
+      cp_async<4>(af + (sw ? 1 : 0), alpha + (size_t)i * D + j);
+      cp_async<4>(af + (sw ? 0 : 1), beta + (size_t)i * D + j);
+      cp_async<8>(&SQ[i * RS + j], carry + (size_t)c * DD + (size_t)i * D + j);
+    } else {
+      *a = ab_pack<DP>(i, 0.0f, 1.0f);
+      SQ[i * RS + j] = make_float2(0.0f, 0.0f);
+    }
     Gs[i * DP + j] = make_float2(0.0f, 0.0f);
   }
+  cp_async_wait_all();
   A[DP * RS + j] = ab_pack<DP>(DP, j == 0 ? 1.0f : 0.0f, 0.0f);
   A[j * RS + DP] = make_float2(0.0f, 0.0f);
   SQ[DP * RS + j] = make_float2(j == 0 ? 1.0f : 0.0f, 0.0f);
