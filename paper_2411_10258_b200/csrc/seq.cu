@@ -249,22 +249,23 @@ k_seq_momsum(int Dp, int64_t C, const float* __restrict__ cmom, float* __restric
 }
 
 // ---------------------------------------------------------------- evaluation workspace
-constexpr int kRedBlocks = 512;   // stage-1 blocks of the chunk reduction (phase 4a)
+// Phase-3 blocks: 4 warps x G chunks each; every block writes one record of partial sums.
+inline int64_t seq_eval_blocks(int Dp, int64_t C) {
+  const int64_t per = 4 * (32 / Dp);
+  return (C + per - 1) / per;
+}
 
 struct SeqWork {
   float2* loc;     // [C][D*D]  local state at chunk end (target-major pairs)
   float2* carry;   // [C][D*D]  state carried into the chunk, anchored at its base
   float2* fin;     // [D*D]     state after the last event, anchored there
-  float2* gpart;   // [C][D*D]  per-chunk (gR, gQ)
-  float* gthp;     // [C][Dp]
-  double* lsp;     // [C]       per-chunk sum lg2 lambda
   float2* gsum;    // [D*D]
   float* gth;      // [Dp]
   double* ls;      // [1]
   int* ctl;        // optimizer control block (seq fit)
   float* prev;     // [D + 2 D^2] previous point (rollback)
   float* opt;      // [2 (D + 2 D^2)] Adam moments when the caller passes none
-  double* rpart;   // [kRedBlocks][2 D^2 + D + 1] stage-1 partial sums
+  double* rpart;   // [phase-3 blocks][2 D^2 + D + 1] per-block partial sums
   size_t bytes;
 };
 
@@ -274,18 +275,14 @@ inline SeqWork make_seq_work(void* base, int D, int Dp, int64_t C) {
   size_t o = 0;
   auto take = [&](size_t nb) { size_t r = o; o = align256(o + nb); return r; };
   const size_t a = take(sizeof(float2) * C * DD), b = take(sizeof(float2) * C * DD),
-               f = take(sizeof(float2) * DD), g = take(sizeof(float2) * C * DD),
-               h = take(sizeof(float) * C * Dp), l = take(sizeof(double) * (C + 1)),
-               gs = take(sizeof(float2) * DD), gt = take(sizeof(float) * Dp), ls = take(sizeof(double)),
+               f = take(sizeof(float2) * DD), gs = take(sizeof(float2) * DD),
+               gt = take(sizeof(float) * Dp), ls = take(sizeof(double)),
                ct = take(sizeof(int) * 64), pv = take(sizeof(float) * P), op = take(sizeof(float) * 2 * P),
-               rp = take(sizeof(double) * kRedBlocks * (2 * DD + D + 1));
+               rp = take(sizeof(double) * (size_t)seq_eval_blocks(Dp, C) * (2 * DD + D + 1));
   char* B = static_cast<char*>(base);
   w.loc = reinterpret_cast<float2*>(B + a);
   w.carry = reinterpret_cast<float2*>(B + b);
   w.fin = reinterpret_cast<float2*>(B + f);
-  w.gpart = reinterpret_cast<float2*>(B + g);
-  w.gthp = reinterpret_cast<float*>(B + h);
-  w.lsp = reinterpret_cast<double*>(B + l);
   w.gsum = reinterpret_cast<float2*>(B + gs);
   w.gth = reinterpret_cast<float*>(B + gt);
   w.ls = reinterpret_cast<double*>(B + ls);
@@ -323,11 +320,11 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
   const int64_t c = ((int64_t)blockIdx.x * 4 + wid) * G + g;
   const bool live = c < C;
   const int n = live ? (int)(cstart[c + 1] - cstart[c]) : 0;
-  for (int i = 0; i < DP; i++) {
-    SQ[j * RS + i] = make_float2(0.0f, 0.0f);
-    // beta_ji: row j, col i
-    if (j < D && i < D) cp_async<4>(&B[j * RS + i], beta + (size_t)j * D + i);
-    else B[j * RS + i] = 0.0f;
+  // lane = column here (coalesced rows of beta): B[r][j] = beta_rj, SQ[r][j] = 0
+  for (int r = 0; r < DP; r++) {
+    SQ[r * RS + j] = make_float2(0.0f, 0.0f);
+    if (r < D && j < D) cp_async<4>(&B[r * RS + j], beta + (size_t)r * D + j);
+    else B[r * RS + j] = 0.0f;
   }
   cp_async_wait_all();
   // column DP: the null event's (never read) column
@@ -368,19 +365,21 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
     load_chunk(c0, tw, dw, mw, min(base + 16, npad));
     local8(c1);
   }
+  // local state at the chunk end, written row by row with lane = column (coalesced): lane j
+  // holds last_j, the anchor of column j
   const float Lc = live ? cspan[c] : 0.0f;
-  for (int i = 0; i < DP; i++) {
-    const float li = __shfl_sync(kFull, last, gbase + i);
-    if (live && j < D && i < D) {
-      float2 s = SQ[j * RS + i];
-      if (li >= 0.0f) {
-        const float dl = Lc - li;
-        const float e = ex2f(B[j * RS + i] * (dl * -kLog2e));
+  __syncwarp();
+  for (int r = 0; r < D; r++) {
+    if (live && j < D) {
+      float2 s = SQ[r * RS + j];
+      if (last >= 0.0f) {
+        const float dl = Lc - last;
+        const float e = ex2f(B[r * RS + j] * (dl * -kLog2e));
         s = make_float2(e * s.x, e * fmaf(dl, s.x, s.y));
       } else {
         s = make_float2(0.0f, 0.0f);
       }
-      loc[(size_t)c * D * D + (size_t)j * D + i] = s;
+      loc[(size_t)c * D * D + (size_t)r * D + j] = s;
     }
   }
 }
@@ -505,8 +504,8 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
            const float* __restrict__ t32, const float* __restrict__ dtp,
            const uint8_t* __restrict__ mk, const float* __restrict__ theta,
            const float* __restrict__ alpha, const float* __restrict__ beta,
-           const float2* __restrict__ carry, float2* __restrict__ gpart, float* __restrict__ gthp,
-           double* __restrict__ lsp, int grad, const int* __restrict__ ctl, int has_history) {
+           const float2* __restrict__ carry, double* __restrict__ rpart, int grad,
+           const int* __restrict__ ctl, int has_history) {
   if (ctl && ctl[0] == 1 && grad) return;
   extern __shared__ __align__(16) unsigned char smem[];
   using SM = Smem<DP>;
@@ -559,59 +558,44 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
     event_loop<DP, false>(A, SQ, Gs, j, gbase, t32, dtp, mk, live ? cbeg[c] : 0, n, nmax, th,
                           last, gth, lsum, last0);
   lsum = group_sum_d<DP>(lsum);
-  if (!live) return;
-  if (j == 0) lsp[c] = lsum;
-  if (grad) {
-    if (j < D) gthp[c * DP + j] = gth;
-    for (int i = 0; i < D; i++)
-      if (j < D) gpart[(size_t)c * DD + (size_t)i * D + j] = Gs[i * DP + j];
-  }
-}
-
-// Phase 4a: fixed-order sums over chunks in two stages (both deterministic).  Elements:
-// 2 D^2 gradient accumulators, D g_theta sums, 1 lsum.  Stage 1: block b sums its contiguous
-// range of chunks for every element (threads over elements: coalesced rows); stage 2: one block
-// sums the kRedBlocks partials per element.
-
-__global__ void __launch_bounds__(256)
-k_seq_reduce1(int D, int Dp, int64_t C, const float2* __restrict__ gpart,
-              const float* __restrict__ gthp, const double* __restrict__ lsp,
-              double* __restrict__ part, int grad, const int* __restrict__ ctl) {
-  if (ctl && ctl[0] == 1 && grad) return;
-  const int DD = D * D, NE = 2 * DD + D + 1;
-  const int64_t per = (C + kRedBlocks - 1) / kRedBlocks;
-  const int64_t c0 = min(C, (int64_t)blockIdx.x * per), c1 = min(C, c0 + per);
+  // Phase 4a, first stage, fused: the block's 4G chunks are summed in a fixed order (fp64) into
+  // one record [2 D^2 gradient accumulators | D g_theta | sum lg2 lambda]; groups past the
+  // last chunk (their loads were clamped to chunk 0's events) are skipped.  Scratch for g_theta
+  // and the lsum: the group's parameter array A (no longer read).
+  float* scf = reinterpret_cast<float*>(A);
+  double* scd = reinterpret_cast<double*>(A + DP);
+  scf[j] = gth;
+  if (j == 0) scd[0] = lsum;
+  __syncthreads();
+  constexpr int NG = 4 * SM::G;   // chunks (groups) per block
+  const int NE = (int)(2 * DD) + D + 1;
   for (int e = threadIdx.x; e < NE; e += blockDim.x) {
     double acc = 0.0;
-    if (e < 2 * DD) {
-      if (grad) {
-        // chunks in order; the loads are independent (unrolled), the adds stay in order
-        const float* gp = reinterpret_cast<const float*>(gpart);
-        int64_t c = c0;
-        for (; c + 4 <= c1; c += 4) {
-          const float v0 = gp[c * 2 * DD + e], v1 = gp[(c + 1) * 2 * DD + e];
-          const float v2 = gp[(c + 2) * 2 * DD + e], v3 = gp[(c + 3) * 2 * DD + e];
-          acc += (double)v0;
-          acc += (double)v1;
-          acc += (double)v2;
-          acc += (double)v3;
+    const int nq = (int)min((int64_t)NG, C - (int64_t)blockIdx.x * NG);
+    for (int q = 0; q < nq; q++) {
+      const float2* gb = reinterpret_cast<const float2*>(smem + (q / SM::G) * SM::per_warp) +
+                         (q % SM::G) * SM::per_group;
+      if (e < (int)(2 * DD)) {
+        if (grad) {
+          const int pr = e >> 1;
+          const float2 v = gb[2 * SM::AS + (pr / D) * DP + (pr % D)];
+          acc += (double)((e & 1) ? v.y : v.x);
         }
-        for (; c < c1; c++) acc += (double)gp[c * 2 * DD + e];
+      } else if (e < (int)(2 * DD) + D) {
+        if (grad) acc += (double)reinterpret_cast<const float*>(gb)[e - (int)(2 * DD)];
+      } else {
+        acc += *reinterpret_cast<const double*>(gb + DP);
       }
-    } else if (e < 2 * DD + D) {
-      if (grad)
-        for (int64_t c = c0; c < c1; c++) acc += (double)gthp[c * Dp + (e - 2 * DD)];
-    } else {
-      for (int64_t c = c0; c < c1; c++) acc += lsp[c];
     }
-    part[(size_t)blockIdx.x * NE + e] = acc;
+    rpart[(size_t)blockIdx.x * NE + e] = acc;
   }
 }
 
-// Stage 2: one warp per element; lane l sums partials l, l+32, ... in order, then a fixed
-// xor-butterfly combines the 32 lane sums (deterministic: the order never depends on timing).
+// Phase 4a, second stage: one warp per element; lane l sums block records l, l+32, ... in
+// order, then a fixed xor-butterfly combines the 32 lane sums (deterministic: the order never
+// depends on timing).  (The first stage, per-block sums over chunks, ends k_seq_eval.)
 __global__ void __launch_bounds__(256)
-k_seq_reduce2(int D, const double* __restrict__ part, float2* __restrict__ gsum,
+k_seq_reduce2(int D, int64_t nblk, const double* __restrict__ part, float2* __restrict__ gsum,
               float* __restrict__ gth, double* __restrict__ ls, int grad, const int* __restrict__ ctl,
               double* __restrict__ raw) {
   if (ctl && ctl[0] == 1 && grad) return;
@@ -620,7 +604,7 @@ k_seq_reduce2(int D, const double* __restrict__ part, float2* __restrict__ gsum,
   if (e >= NE) return;
   double acc = 0.0;
 #pragma unroll 4
-  for (int q = lane; q < kRedBlocks; q += 32) acc += part[(size_t)q * NE + e];
+  for (int64_t q = lane; q < nblk; q += 32) acc += part[(size_t)q * NE + e];
   for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
   if (lane != 0) return;
   if (raw) raw[e] = acc;   // f1: the slice's exact partial sums, all-reduced across ranks
@@ -894,8 +878,8 @@ static void seq_phases_t(const SeqLayout& L, const void* pk, const float* th, co
   const size_t smem = 4 * SM::per_warp;
   k_seq_eval<DP><<<blk, 128, smem, st>>>(L.D, C, at<int64_t>(pk, L.cstart), at<int64_t>(pk, L.cbeg),
                                          at<float>(pk, L.t32), at<float>(pk, L.dtp),
-                                         at<uint8_t>(pk, L.mark), th, al, be, w.carry, w.gpart,
-                                         w.gthp, w.lsp, grad, ctl, has_history);
+                                         at<uint8_t>(pk, L.mark), th, al, be, w.carry, w.rpart,
+                                         grad, ctl, has_history);
   count_launch();
 }
 
@@ -942,11 +926,10 @@ static void seq_phases(const SeqLayout& L, const void* pk, const float* th, cons
 static void seq_reduce(const SeqLayout& L, const SeqWork& w, int grad, const int* ctl,
                        cudaStream_t st, double* raw = nullptr) {
   if (L.C == 0) return;
-  k_seq_reduce1<<<kRedBlocks, 256, 0, st>>>(L.D, L.Dp, L.C, w.gpart, w.gthp, w.lsp, w.rpart, grad,
-                                            ctl);
   const int ne = 2 * L.D * L.D + L.D + 1;
-  k_seq_reduce2<<<(ne + 7) / 8, 256, 0, st>>>(L.D, w.rpart, w.gsum, w.gth, w.ls, grad, ctl, raw);
-  count_launch(2);
+  k_seq_reduce2<<<(ne + 7) / 8, 256, 0, st>>>(L.D, seq_eval_blocks(L.Dp, L.C), w.rpart, w.gsum,
+                                              w.gth, w.ls, grad, ctl, raw);
+  count_launch(1);
 }
 
 static size_t seq_work_bytes(const SeqLayout& L) {
