@@ -561,6 +561,11 @@ def main():
     mio_ach = ev_it_step * mio_per_ev / (fit_avg / 1e3) / 1e9
     mio = {"achieved_Gslots": mio_ach, "peak_Gslots": mio_peak, "frac": mio_ach / mio_peak,
            "per_unit": f"{mio_per_ev:.3f} MIO slots per event-iteration (shared wavefronts + shuffles)"}
+    if Dp == 16:
+        # the same pipe measured by ncu on this kernel (all shared wavefronts incl. the
+        # non-loop phases, plus SHFL), not the algorithmic count above
+        mio["ncu_measured_frac"] = 0.803
+        mio["ncu_source"] = "profiles/r01_k_fit_v10_wavefronts.txt (16,384 windows x 101 evaluations)"
     roof = {"bound": "alu", "achieved": achieved, "peak": MUFU_PEAK_GOPS, "unit": "Gop/s (MUFU)",
             "frac": achieved / MUFU_PEAK_GOPS, "traffic": traffic, "kernel": f"k_fit<{Dp}>",
             "per_unit": f"{mufu_per_ev} MUFU ops per event-iteration (2D ex2 + lg2 + rcp)",
