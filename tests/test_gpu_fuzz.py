@@ -1,0 +1,139 @@
+"""Randomised GPU parity sweep over EVERY D in 1..32 (each padded width DP and each D < DP
+padding case), against the fp64 oracle on the same seeded inputs (R17 bars).
+
+Windows are drawn to stress the layout rather than to look like traffic: lengths 0, 1, 2, a few
+hundred, and an occasional long window among short ones (ragged warps, long-first order);
+skewed or absent marks; cross-mark ties (allowed, R2/R10); events at exactly 0 and T; horizons
+from 0.5 to 40; parameters spanning small and large beta*u (both compensator branches)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2411_10258_b200 as M
+from paper_2411_10258_b200 import mdhp
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def f32(x):
+    return np.asarray(x, np.float32)
+
+
+def fuzz_windows(rng, D, W):
+    wins, Ts = [], []
+    for w in range(W):
+        T = float(rng.choice([0.5, 1.0, 3.0, 40.0]))
+        kind = rng.integers(0, 8)
+        n = [0, 1, 2, int(rng.integers(3, 60)), int(rng.integers(60, 300)), int(rng.integers(60, 300)),
+             int(rng.integers(3, 120)), 700 if w == 1 else int(rng.integers(3, 40))][kind]
+        # skewed marks; some marks never occur
+        p = rng.dirichlet(np.full(D, 0.4))
+        m = rng.choice(D, size=n, p=p).astype(np.int32)
+        t = np.sort(rng.uniform(0.0, T, n))
+        if n >= 4:
+            t[0] = 0.0                      # an event at the window origin
+            if rng.random() < 0.5:
+                t[-1] = T                   # and one at the horizon
+            for k in range(1, n - 1, 5):    # cross-mark ties
+                if m[k] != m[k - 1]:
+                    t[k] = t[k - 1]
+        wins.append((t, m))
+        Ts.append(T)
+    return H.batch_from_windows(wins, np.array(Ts))
+
+
+def fuzz_params(rng, W, D):
+    th = rng.uniform(0.05, 20.0, (W, D))
+    al = rng.uniform(0.0, 3.0, (W, D, D)) * (rng.random((W, D, D)) < 0.7)   # some exact zeros
+    be = np.exp(rng.uniform(np.log(1e-3), np.log(80.0), (W, D, D)))          # both compensator branches
+    return th, al, be
+
+
+@pytest.mark.parametrize("D", list(range(1, 33)))
+def test_fuzz_loglik_all_D(D):
+    rng = np.random.default_rng(9000 + D)
+    W = int(rng.integers(5, 28))
+    b = fuzz_windows(rng, D, W)
+    th, al, be = fuzz_params(rng, W, D)
+    dev = (torch.tensor(b["t"], dtype=torch.float64, device=DEV), torch.tensor(b["mark"], dtype=torch.int32, device=DEV),
+           torch.tensor(b["win_off"], dtype=torch.int64, device=DEV), torch.tensor(b["T"], dtype=torch.float64, device=DEV))
+    pk = M.pack_windows(D, *dev)
+    r = M.loglik_grad(pk, torch.tensor(f32(th), device=DEV), torch.tensor(f32(al), device=DEV),
+                      torch.tensor(f32(be), device=DEV))
+    torch.cuda.synchronize()
+    out = {k: v.cpu().numpy() for k, v in r.items() if v is not None}
+    t32, T32, st = H.oracle_times(b, D)
+    assert np.array_equal(pk.status.cpu().numpy()[:W] & ~mdhp.ST_EMPTY, st & ~mdhp.ST_EMPTY)
+    for w in range(W):
+        a, z = b["win_off"][w], b["win_off"][w + 1]
+        p = (f32(th[w]).astype(float), f32(al[w]).astype(float), f32(be[w]).astype(float))
+        ref = oracle.loglik_rec(D, t32[a:z], b["mark"][a:z], T32[w], *p)
+        rel = abs(out["lnl"][w] - ref["lnl"]) / max(abs(ref["lnl"]), 1e-300)
+        assert rel <= 1e-4, (D, w, z - a, out["lnl"][w], ref["lnl"])
+        sth, sal, sbe = H.grad_scales(t32[a:z], b["mark"][a:z], T32[w], *p, ref)
+        H.assert_grad_close(out["g_theta"][w], ref["g_theta"], sth, what=f"D{D} w{w} theta")
+        H.assert_grad_close(out["g_alpha"][w], ref["g_alpha"], sal, what=f"D{D} w{w} alpha")
+        H.assert_grad_close(out["g_beta"][w], ref["g_beta"], sbe, what=f"D{D} w{w} beta")
+
+
+@pytest.mark.parametrize("D", [4, 7, 11, 23, 31])
+def test_fuzz_fit_adam_all_widths(D):
+    """5 Adam iterations from random starts: parameters within 1e-3 (R17) of the oracle's fit."""
+    rng = np.random.default_rng(9100 + D)
+    W = 12
+    b = fuzz_windows(rng, D, W)
+    th, al, be = fuzz_params(rng, W, D)
+    be = np.clip(be, 0.05, None)    # keep the first Adam steps away from the projection floor
+    dev = (torch.tensor(b["t"], dtype=torch.float64, device=DEV), torch.tensor(b["mark"], dtype=torch.int32, device=DEV),
+           torch.tensor(b["win_off"], dtype=torch.int64, device=DEV), torch.tensor(b["T"], dtype=torch.float64, device=DEV))
+    pk = M.pack_windows(D, *dev)
+    tht, alt, bet = (torch.tensor(f32(x), device=DEV) for x in (th, al, be))
+    M.fit(pk, tht, alt, bet, M.FitConfig(max_iters=5, optimizer="adam", lr=0.02, tol_rel=0.0))
+    torch.cuda.synchronize()
+    g = {"theta": tht.cpu().numpy(), "alpha": alt.cpu().numpy(), "beta": bet.cpu().numpy()}
+    t32, T32, _ = H.oracle_times(b, D)
+    ocfg = oracle.FitConfig(max_iters=5, optimizer="adam", lr=0.02, tol_rel=0.0)
+    for w in range(W):
+        a, z = b["win_off"][w], b["win_off"][w + 1]
+        o = oracle.fit(D, t32[a:z], b["mark"][a:z], T32[w], f32(th[w]).astype(float),
+                       f32(al[w]).astype(float), f32(be[w]).astype(float), ocfg)
+        for k in ("theta", "alpha", "beta"):
+            ref = o[k]
+            s = 1e-2 * max(np.mean(np.abs(ref)), 1e-4)
+            bad = np.abs(g[k][w] - ref) > 1e-3 * np.maximum(np.abs(ref), s)
+            assert not bad.any(), (D, w, k, np.argwhere(bad)[:3].tolist(), g[k][w][bad][:3], ref[bad][:3])
+
+
+@pytest.mark.parametrize("D,ce", [(2, 8), (5, 24), (7, 200), (24, 64), (32, 40)])
+def test_fuzz_sequence_path(D, ce):
+    """The chunked-scan path (a7) on one fuzzed sequence (ties, skewed marks, events at 0 and T)
+    against the oracle's eager recursion on the fp64 times (R19)."""
+    rng = np.random.default_rng(9200 + D)
+    T = 30.0
+    n = 2500
+    p = rng.dirichlet(np.full(D, 0.5))
+    m = rng.choice(D, size=n, p=p).astype(np.int32)
+    t = np.sort(rng.uniform(0.0, T, n))
+    t[0], t[-1] = 0.0, T
+    for k in range(1, n - 1, 7):
+        if m[k] != m[k - 1]:
+            t[k] = t[k - 1]
+    th, al, be = (x[0] for x in fuzz_params(rng, 1, D))
+    be = np.clip(be, 0.05, None)
+    ps = M.seq_pack(D, torch.tensor(t, dtype=torch.float64, device=DEV), torch.tensor(m, dtype=torch.int32, device=DEV),
+                    T, chunk_events=ce)
+    r = M.seq_loglik_grad(ps, torch.tensor(f32(th), device=DEV), torch.tensor(f32(al), device=DEV),
+                          torch.tensor(f32(be), device=DEV))
+    torch.cuda.synchronize()
+    out = {k: v.cpu().numpy() for k, v in r.items() if v is not None}
+    prm = (f32(th).astype(float), f32(al).astype(float), f32(be).astype(float))
+    ref = oracle.loglik_rec(D, t, m, T, *prm)
+    rel = abs(out["lnl"][0] - ref["lnl"]) / abs(ref["lnl"])
+    assert rel <= 1e-4, (D, ce, out["lnl"][0], ref["lnl"])
+    sth, sal, sbe = H.grad_scales(t, m, T, *prm, ref)
+    H.assert_grad_close(out["g_theta"], ref["g_theta"], sth, what=f"seq D{D} theta")
+    H.assert_grad_close(out["g_alpha"], ref["g_alpha"], sal, what=f"seq D{D} alpha")
+    H.assert_grad_close(out["g_beta"], ref["g_beta"], sbe, what=f"seq D{D} beta")
