@@ -661,6 +661,17 @@ k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
   const int j = tid % D;
   const bool pair = tid < DD;
   if (tid == 0) okflag = 1;
+  // everything this thread may need, loaded up front (one memory round trip instead of a
+  // chain: parameters, and in a fit step the Adam moments of its theta/alpha/beta entries)
+  const float a_cur = pair ? alpha[tid] : 0.0f, b_cur = pair ? beta[tid] : 1.0f;
+  const float th_cur = tid < D ? theta[tid] : 0.0f;
+  const size_t P = (size_t)D + 2 * (size_t)DD;
+  const bool adam_step = ctl && grad && cfg.optimizer == MDHP_OPT_ADAM;
+  float mth = 0.0f, vth = 0.0f, ma = 0.0f, va = 0.0f, mb = 0.0f, vb = 0.0f;
+  if (adam_step) {
+    if (tid < D) { mth = opt[tid]; vth = opt[P + tid]; }
+    if (pair) { ma = opt[D + tid]; va = opt[P + D + tid]; mb = opt[D + DD + tid]; vb = opt[P + D + DD + tid]; }
+  }
   __syncthreads();
   double part3 = 0.0;
   float da = 0.0f, db = 0.0f;
@@ -673,7 +684,7 @@ k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
     ci.umax = umax[j];
     Series S;
     load_series(S, mom + (size_t)j * kMom, ci.N > 0);
-    const float a = alpha[tid], b = beta[tid];
+    const float a = a_cur, b = b_cur;
     const float2 f = fin[tid];
     float Eb, Hb2;
     compensator(ci, S, b, f.x, f.y, Eb, Hb2);
@@ -685,7 +696,7 @@ k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
       if (!isfinite(da) || !isfinite(db)) okflag = 0;
     }
   }
-  double sth = (tid < D) ? (double)theta[tid] : 0.0;
+  double sth = (tid < D) ? (double)th_cur : 0.0;
   float dth = 0.0f;
   if (grad && tid < D) {
     dth = gthv[tid] - (float)T;
@@ -713,9 +724,10 @@ k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
     }
     return;
   }
-  const size_t P = (size_t)D + 2 * (size_t)DD;
   const bool finite = okflag && isfinite(lnl);
   __shared__ int act;   // 0 = stop, 1 = step, 2 = rollback
+  __shared__ float lr_s;
+  __shared__ int s_s;
   if (tid == 0) {
     act = 0;
     if (!finite) {
@@ -750,6 +762,8 @@ k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
         act = 1;
       }
     }
+    lr_s = ctl->lr_w;
+    s_s = ctl->s;
   }
   __syncthreads();
   if (act == 2) {   // roll back to the previous point
@@ -760,22 +774,22 @@ k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
     }
   } else if (act == 1) {
     // save the previous point, then step
-    if (tid < D) prev[tid] = theta[tid];
+    if (tid < D) prev[tid] = th_cur;
     if (pair) {
-      prev[D + tid] = alpha[tid];
-      prev[D + DD + tid] = beta[tid];
+      prev[D + tid] = a_cur;
+      prev[D + DD + tid] = b_cur;
     }
-    const float lr_w = ctl->lr_w;
-    const int s = ctl->s;
+    const float lr_w = lr_s;
+    const int s = s_s;
     const float scale = (cfg.loss_mean && n_events > 0) ? 1.0f / (float)n_events : 1.0f;
     const bool adam = cfg.optimizer == MDHP_OPT_ADAM;
     const float bc1 = adam ? 1.0f - powf(cfg.b1, (float)s) : 1.0f;
     const float sbc2 = adam ? sqrtf(1.0f - powf(cfg.b2, (float)s)) : 1.0f;
-    auto upd = [&](float p, float g, size_t q, float lo) -> float {
+    auto upd = [&](float p, float g, size_t q, float m0, float v0, float lo) -> float {
       const float gl = -g * scale;
       if (adam) {
-        const float mm = cfg.b1 * opt[q] + (1.0f - cfg.b1) * gl;
-        const float vv = cfg.b2 * opt[P + q] + (1.0f - cfg.b2) * gl * gl;
+        const float mm = cfg.b1 * m0 + (1.0f - cfg.b1) * gl;
+        const float vv = cfg.b2 * v0 + (1.0f - cfg.b2) * gl * gl;
         opt[q] = mm;
         opt[P + q] = vv;
         p = p - (lr_w / bc1) * (mm / (sqrtf(vv) / sbc2 + cfg.eps));
@@ -784,18 +798,18 @@ k_seq_finish(int D, int Dp, double T, const float* __restrict__ tail,
       }
       return p < lo ? lo : p;
     };
-    if (tid < D && (cfg.fit_mask & MDHP_FIT_THETA)) theta[tid] = upd(theta[tid], dth, tid, cfg.min_param);
+    if (tid < D && (cfg.fit_mask & MDHP_FIT_THETA))
+      theta[tid] = upd(th_cur, dth, tid, mth, vth, cfg.min_param);
     if (pair) {
-      if (cfg.fit_mask & MDHP_FIT_ALPHA) alpha[tid] = upd(alpha[tid], da, D + tid, 0.0f);
-      if (cfg.fit_mask & MDHP_FIT_BETA) beta[tid] = upd(beta[tid], db, D + DD + tid, cfg.min_param);
+      if (cfg.fit_mask & MDHP_FIT_ALPHA) alpha[tid] = upd(a_cur, da, D + tid, ma, va, 0.0f);
+      if (cfg.fit_mask & MDHP_FIT_BETA) beta[tid] = upd(b_cur, db, D + DD + tid, mb, vb, cfg.min_param);
     }
   }
-  __syncthreads();
-  if (tid == 0 && act == 1) {
-    ctl->it++;
+  // only thread 0 touches the control block
+  if (tid == 0) {
+    if (act == 1) ctl->it++;
+    if (ctl->it >= cfg.max_iters) ctl->done = 1;
   }
-  __syncthreads();
-  if (tid == 0 && ctl->it >= cfg.max_iters) ctl->done = 1;
 }
 
 // ---------------------------------------------------------------- host side
