@@ -51,7 +51,8 @@ def parse():
     ap.add_argument("--tol", type=float, default=0.0,
                     help="converged mode (SURVEY 8(d)): tol_rel (e.g. 1e-6, patience 10, capped at --iters); "
                          "0 = fixed-iteration mode (the headline)")
-    ap.add_argument("--chunk", type=int, default=256, help="--config cfg4: events per chunk")
+    ap.add_argument("--chunk", type=int, default=0,
+                    help="--config cfg4: events per chunk (0: mdhp_seq_chunk_hint, whole waves)")
     ap.add_argument("--hidden", type=int, default=128, help="--config feat: MDHP-LSTM hidden size H")
     ap.add_argument("--shard-seq", action="store_true",
                     help="cfg4: split ONE sequence over the ranks (f1, strong scaling, NCCL map exchange)")
@@ -231,7 +232,8 @@ def bench_seq(args, rc, world, rank, dev):
         return bench_seq_sharded(args, rc, world, rank, dev)
     b = sgpu.make_batch_gpu(rc, 1, seed=args.seed, first_window=rank, device=dev)
     N = int(b["win_off"][-1])
-    ps = M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=args.chunk)
+    ce = args.chunk or M.seq_chunk_hint(D, N)
+    ps = M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=ce)
     th0 = b["theta"][0].clone(); al0 = b["alpha"][0].clone(); be0 = b["beta"][0].clone()
     th, al, be = th0.clone(), al0.clone(), be0.clone()
     cfg = M.FitConfig(max_iters=args.iters, optimizer="adam", lr=0.05, tol_rel=0.0)
@@ -239,7 +241,7 @@ def bench_seq(args, rc, world, rank, dev):
 
     def step():
         th.copy_(th0); al.copy_(al0); be.copy_(be0)
-        M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=args.chunk, out=ps)
+        M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=ce, out=ps)
         return M.seq_fit(ps, th, al, be, cfg)
     for _ in range(args.warmup):
         r = step()
@@ -265,7 +267,7 @@ def bench_seq(args, rc, world, rank, dev):
                           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                           "data": f"synthetic (Ogata-thinned MDHP on GPU, recipe cfg4, seed {args.seed})",
                           "config": {"workload": f"cfg4: one sequence/GPU, D={D}, {N} events over {rc.T}s, "
-                                                 f"chunked scan ({args.chunk} events/chunk), Adam lr 0.05, {args.iters} "
+                                                 f"chunked scan ({ce} events/chunk{'' if args.chunk else ', mdhp_seq_chunk_hint'}), Adam lr 0.05, {args.iters} "
                                                  "fixed iterations + final eval", "events": N},
                           "gpu_launches": int(M.launch_count() - L0)}), flush=True)
     if world > 1:

@@ -237,6 +237,15 @@ typedef struct {
 
 size_t mdhp_seq_packed_bytes(const mdhp_seq_desc* desc);
 
+/* A chunk_events value for an N-event sequence of D marks on the CURRENT device: the smallest
+ * size (>= 8) whose chunks fill whole waves of the phase-3 kernel (SM count x its occupancy x
+ * chunks per warp), so no SM runs one more block than the others in a partial last wave
+ * (a chunk never exceeds chunk_events events, tie groups aside, so ceil(N / size) bounds the
+ * chunk count).  At least 256 events per chunk once a wave is full.  Returns the size, or a
+ * negative MDHP_E* code (EDIM: D outside 1..32 or N < 0; ECUDA).  Host-only, synchronous.
+ * Not in the paper: a launch-shape helper for the chunked scan of row a7.                    */
+int32_t mdhp_seq_chunk_hint(int32_t D, int64_t n_events);
+
 /* t [N] fp64 non-decreasing in [0, T], mark [N] int32 in 0..D-1 (device).  status [1] int32
  * (device) receives the MDHP_ST_* validation bits.  Asynchronous.                          */
 int mdhp_seq_pack(const mdhp_seq_desc* desc, const double* t, const int32_t* mark,

@@ -6,9 +6,9 @@ GPU every call raises.
 """
 from .mdhp import (FitConfig, Packed, PackedSeq, fit, fit_host, hawkes_features,  # noqa: F401
                    launch_count, lib, loglik_dense, loglik_grad, make_desc, pack_windows,
-                   packed_bytes, seq_fit, seq_loglik_grad, seq_pack)
+                   packed_bytes, seq_chunk_hint, seq_fit, seq_loglik_grad, seq_pack)
 from . import mdhp  # noqa: F401
 
 __all__ = ["FitConfig", "Packed", "PackedSeq", "fit", "fit_host", "hawkes_features", "launch_count", "lib",
            "loglik_dense", "loglik_grad",
-           "make_desc", "pack_windows", "packed_bytes", "seq_fit", "seq_loglik_grad", "seq_pack", "mdhp"]
+           "make_desc", "pack_windows", "packed_bytes", "seq_chunk_hint", "seq_fit", "seq_loglik_grad", "seq_pack", "mdhp"]

@@ -48,6 +48,7 @@ int seq_fit_launch(int D, int64_t N, int ce, double T, const void* pk, const Fit
                    float* th, float* al, float* be, float* opt_state, double* lnl, int32_t* iters,
                    int32_t* status, float* trace, cudaStream_t st);
 size_t seq_packed_bytes(int D, int64_t N, int ce);
+int seq_chunk_hint(int D, int64_t N);
 
 static thread_local char g_err[512] = "";
 static std::atomic<uint64_t> g_launches{0};
@@ -334,6 +335,16 @@ int mdhp_fit(const mdhp_pack_desc* d, const void* packed, const mdhp_fit_config*
 size_t mdhp_seq_packed_bytes(const mdhp_seq_desc* d) {
   if (check_seq(d) != MDHP_OK) return 0;
   return seq_packed_bytes(d->D, d->n_events, d->chunk_events);
+}
+
+int32_t mdhp_seq_chunk_hint(int32_t D, int64_t n_events) {
+  if (D < 1 || D > 32 || n_events < 0) {
+    set_error("bad sequence dims (D=%d, N=%lld)", D, (long long)n_events);
+    return MDHP_EDIM;
+  }
+  const int ce = seq_chunk_hint(D, n_events);
+  if (ce < 0) set_error("mdhp_seq_chunk_hint: CUDA error");
+  return ce;
 }
 
 int mdhp_seq_pack(const mdhp_seq_desc* d, const double* t, const int32_t* mark, void* packed,

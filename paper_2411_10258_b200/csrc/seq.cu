@@ -16,6 +16,7 @@
 // Chunk-relative fp32 times (fp64 base per chunk) keep ~1e-7 s resolution over 1000 s.
 #include <cmath>
 #include <cstdlib>
+#include <algorithm>
 #include "eval.cuh"
 
 namespace mdhp {
@@ -921,6 +922,37 @@ static void seq_set_attrs(const SeqLayout& L) {
     case 16: seq_set_attrs_t<16>(); break;
     case 32: seq_set_attrs_t<32>(); break;
   }
+}
+
+// Balanced chunk size (mdhp_seq_chunk_hint): phase 3 holds 4 warps x G chunks per block; fill
+// whole waves of SMs x resident blocks.
+template <int DP>
+static int seq_chunk_hint_t(int64_t N) {
+  seq_set_attrs_t<DP>();
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_seq_eval<DP>, 128,
+                                                     4 * Smem<DP>::per_warp) != cudaSuccess)
+    return MDHP_ECUDA;
+  const int64_t wave = (int64_t)sms * (per_sm > 0 ? per_sm : 1) * 4 * (32 / DP);   // chunks
+  const int64_t waves = (N + wave * 256 - 1) / (wave * 256);
+  const int64_t ce = waves > 0 ? (N + wave * waves - 1) / (wave * waves) : 256;
+  return (int)std::min<int64_t>(std::max<int64_t>(ce, 8), 1 << 30);
+}
+
+int seq_chunk_hint(int D, int64_t N) {
+  int dp = 1;
+  while (dp < D) dp <<= 1;
+  switch (dp) {
+    case 1: return seq_chunk_hint_t<1>(N);
+    case 2: return seq_chunk_hint_t<2>(N);
+    case 4: return seq_chunk_hint_t<4>(N);
+    case 8: return seq_chunk_hint_t<8>(N);
+    case 16: return seq_chunk_hint_t<16>(N);
+    case 32: return seq_chunk_hint_t<32>(N);
+  }
+  return MDHP_EDIM;
 }
 
 static void seq_phases(const SeqLayout& L, const void* pk, const float* th, const float* al,

@@ -102,6 +102,8 @@ def lib() -> ctypes.CDLL:
                                     P, P, P, P, P, P, P]
         L.mdhp_seq_packed_bytes.restype = ctypes.c_size_t
         L.mdhp_seq_packed_bytes.argtypes = [ctypes.POINTER(SeqDesc)]
+        L.mdhp_seq_chunk_hint.restype = ctypes.c_int32
+        L.mdhp_seq_chunk_hint.argtypes = [ctypes.c_int32, ctypes.c_int64]
         L.mdhp_seq_pack.restype = ctypes.c_int
         L.mdhp_seq_pack.argtypes = [ctypes.POINTER(SeqDesc), P, P, P, ctypes.c_size_t, P, P]
         L.mdhp_seq_loglik_grad.restype = ctypes.c_int
@@ -335,11 +337,21 @@ class PackedSeq:
         return int(self.desc.D)
 
 
+def seq_chunk_hint(D, n_events) -> int:
+    """mdhp_seq_chunk_hint: a chunk size whose chunks fill whole waves of the current device."""
+    ce = int(lib().mdhp_seq_chunk_hint(int(D), int(n_events)))
+    if ce < 0:
+        _check(ce, "mdhp_seq_chunk_hint")
+    return ce
+
+
 def seq_pack(D, t, mark, T, chunk_events=256, out: PackedSeq | None = None, t0=0.0, has_history=False,
              stream=None) -> PackedSeq:
     """mdhp_seq_pack on CUDA tensors t f64[N], mark i32[N] (one sequence on [0, T], or one slice of
-    it starting after t0 when has_history)."""
+    it starting after t0 when has_history).  chunk_events=0: mdhp_seq_chunk_hint."""
     _dev(t, torch.float64, "t"); _dev(mark, torch.int32, "mark")
+    if not chunk_events:
+        chunk_events = seq_chunk_hint(D, t.numel())
     desc = SeqDesc(int(D), int(chunk_events), int(t.numel()), float(T), float(t0), int(bool(has_history)), 0)
     nb = int(lib().mdhp_seq_packed_bytes(ctypes.byref(desc)))
     if nb == 0:

@@ -65,6 +65,9 @@ def test_bad_arguments_rejected_without_gpu():
     c = M.FitConfig(lr=-1.0).c()
     assert L.mdhp_fit(ctypes.byref(d), fake, ctypes.byref(c), fake, fake, fake, None, fake, fake,
                       fake, None, None) == -1
+    # the chunk-size hint validates its dimensions before touching the device
+    assert L.mdhp_seq_chunk_hint(0, 100) == -2 and L.mdhp_seq_chunk_hint(33, 100) == -2
+    assert L.mdhp_seq_chunk_hint(4, -1) == -2
 
 
 def test_layout_is_pure_function():

@@ -137,3 +137,23 @@ def test_fuzz_sequence_path(D, ce):
     H.assert_grad_close(out["g_theta"], ref["g_theta"], sth, what=f"seq D{D} theta")
     H.assert_grad_close(out["g_alpha"], ref["g_alpha"], sal, what=f"seq D{D} alpha")
     H.assert_grad_close(out["g_beta"], ref["g_beta"], sbe, what=f"seq D{D} beta")
+
+
+def test_chunk_hint_is_a_valid_chunk_size():
+    """mdhp_seq_chunk_hint: a usable size; packing with it gives the same lnL as a fixed size."""
+    assert M.seq_chunk_hint(16, 0) >= 8 and M.seq_chunk_hint(3, 100) >= 8
+    rng = np.random.default_rng(9300)
+    D, T, n = 16, 200.0, 40000
+    m = rng.integers(0, D, n).astype(np.int32)
+    t = np.sort(rng.uniform(0.0, T, n))
+    th, al, be = (x[0] for x in fuzz_params(rng, 1, D))
+    be = np.clip(be, 0.5, None)
+    ce = M.seq_chunk_hint(D, n)
+    assert 8 <= ce <= n
+    args = [torch.tensor(f32(x), device=DEV) for x in (th, al, be)]
+    lnl = []
+    for c in (ce, 64, 0):
+        ps = M.seq_pack(D, torch.tensor(t, dtype=torch.float64, device=DEV),
+                        torch.tensor(m, dtype=torch.int32, device=DEV), T, chunk_events=c)
+        lnl.append(float(M.seq_loglik_grad(ps, *args, grads=False)["lnl"][0]))
+    assert lnl[0] == pytest.approx(lnl[1], rel=1e-5) and lnl[2] == lnl[0]
