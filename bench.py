@@ -186,7 +186,7 @@ def bench_seq_sharded(args, rc, world, rank, dev):
 
     def step():
         ctx = seqdist.make_slice(D, b["t"][lo:hi].contiguous(), b["mark"][lo:hi].contiguous(), rc.T, t0,
-                                 rank, chunk_events=256, cfg=cfg)
+                                 rank, chunk_events=args.chunk, cfg=cfg)
         p = {"theta": th0.clone(), "alpha": al0.clone(), "beta": be0.clone()}
         return seqdist.fit([ctx], comm, [p], cfg, n_total=N)[0]
     for _ in range(args.warmup):
