@@ -350,3 +350,28 @@ def test_very_long_window_among_short_ones():
         H.assert_grad_close(got["g_theta"][w], ref["g_theta"], sth, what=f"w{w} theta")
         H.assert_grad_close(got["g_alpha"][w], ref["g_alpha"], sal, what=f"w{w} alpha")
         H.assert_grad_close(got["g_beta"][w], ref["g_beta"], sbe, what=f"w{w} beta")
+
+
+def test_fit_nonfinite_rollback_and_divergence_match_oracle():
+    """The non-finite branch of the fit loop: a GD step with lr = inf makes every
+    parameter +-inf or NaN in fp32 and fp64 alike (IEEE), the next evaluation is non-finite, the
+    point is rolled back and lr halved (still inf) until the halving budget is spent, then the
+    window is DIVERGED at its last finite point.  Status bits, iteration counts, parameters and
+    lnL must equal the oracle's, window by window."""
+    D = 4
+    b, (th, al, be) = H.small_batch(D, 6, seed=505, edges=True)
+    W = len(b["T"])
+    for halvings in (0, 3):
+        kw = dict(max_iters=50, optimizer="gd", lr=float("inf"), tol_rel=0.0, max_halvings=halvings)
+        g, o = _fit_both(D, b, th, al, be, M.FitConfig(**kw), oracle.FitConfig(**kw))
+        for w in range(W):
+            assert g["status"][w] & mdhp.ST_DIVERGED and o[w]["status"] & mdhp.ST_DIVERGED, w
+            assert (g["status"][w] & (mdhp.ST_NONFINITE | mdhp.ST_DIVERGED)) == \
+                (o[w]["status"] & (mdhp.ST_NONFINITE | mdhp.ST_DIVERGED))
+            assert int(g["iters"][w]) == o[w]["iters"], (w, g["iters"][w], o[w]["iters"])
+            # the returned point is the last finite one: the (fp32) starting point
+            np.testing.assert_array_equal(g["theta"][w], f32(th[w]))
+            np.testing.assert_array_equal(g["alpha"][w], f32(al[w]))
+            np.testing.assert_array_equal(g["beta"][w], f32(be[w]))
+            np.testing.assert_array_equal(o[w]["alpha"], f32(al[w]).astype(float))
+            assert abs(g["lnl"][w] - o[w]["lnl"]) <= 1e-4 * abs(o[w]["lnl"])
