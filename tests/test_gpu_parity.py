@@ -375,3 +375,23 @@ def test_fit_nonfinite_rollback_and_divergence_match_oracle():
             np.testing.assert_array_equal(g["beta"][w], f32(be[w]))
             np.testing.assert_array_equal(o[w]["alpha"], f32(al[w]).astype(float))
             assert abs(g["lnl"][w] - o[w]["lnl"]) <= 1e-4 * abs(o[w]["lnl"])
+
+
+@pytest.mark.parametrize("mask", [2, 4, 5, 6])
+def test_fit_masks_and_adam_hyperparameters(mask):
+    """Frozen parameter groups (fit_mask: 1 theta, 2 alpha, 4 beta) keep their start values bit
+    for bit; the fitted groups follow the oracle within R17 under non-default Adam
+    hyper-parameters (b1, b2, eps) and the MEAN loss."""
+    D = 5
+    b, (th, al, be) = H.small_batch(D, 8, seed=600 + mask, edges=False)
+    W = len(b["T"])
+    th0, al0, be0 = th * 1.3, al * 0.7 + 0.05, be * 1.2
+    kw = dict(max_iters=12, optimizer="adam", lr=0.03, b1=0.8, b2=0.99, eps=1e-6, loss="mean",
+              tol_rel=0.0, fit_mask=mask)
+    g, o = _fit_both(D, b, th0, al0, be0, M.FitConfig(**kw), oracle.FitConfig(**kw))
+    for w in range(W):
+        for k, bit, start in (("theta", 1, th0), ("alpha", 2, al0), ("beta", 4, be0)):
+            if mask & bit:
+                _param_close(g[k][w], o[w][k], what=f"mask{mask} w{w} {k}")
+            else:
+                np.testing.assert_array_equal(g[k][w], f32(start[w]))
