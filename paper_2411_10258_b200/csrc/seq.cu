@@ -388,8 +388,8 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
 // Phase 2: exclusive scan of the per-chunk affine maps.  Block = kScanP pairs x kScanS segments
 // of chunks (thread = (segment, pair), pair fastest: a warp's loads of a chunk's pair row fill
 // whole 32-byte sectors); each thread composes its segment in order, the segment maps are
-// scanned across the block in log2(kScanS) rounds, then each thread re-walks its segment writing
-// the carried states.  (kScanP = 32 with 32 segments was measured 2x slower: too few blocks.)
+// scanned across the block (warp shuffles, then a scan of the warp totals), then each thread
+// re-walks its segment writing the carried states.  (kScanP = 32 with 32 segments was measured 2x slower: too few blocks.)
 struct AffMap {
   float E, L, Sb, Qb;
 };
@@ -416,7 +416,7 @@ k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __res
            const float* __restrict__ spans, int rank, float2* __restrict__ rankmap,
            float* __restrict__ rankspan, int maps_only) {
   if (ctl && ctl[0]) return;
-  __shared__ AffMap sm[kScanS][kScanP];
+  __shared__ AffMap sm[32][kScanP];   // per-warp totals (32 warps of 1024 threads)
   const int lane = threadIdx.x % kScanP, seg = threadIdx.x / kScanP;
   const int64_t DD = (int64_t)D * D;
   const int64_t p = (int64_t)blockIdx.x * kScanP + lane;
@@ -446,16 +446,36 @@ k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __res
       }
     }
   }
-  sm[seg][lane] = m;
-  __syncthreads();
-  for (int o = 1; o < kScanS; o <<= 1) {   // inclusive Hillis-Steele scan over the segments
-    AffMap prev = m;
-    if (seg >= o) prev = compose(sm[seg - o][lane], m);
-    __syncthreads();
-    m = prev;
-    sm[seg][lane] = m;
-    __syncthreads();
+  // inclusive scan of the segment maps (per pair, over segments) in two levels: shuffles
+  // within each warp (32 / kScanP segments), then one warp per pair scans the 32 warp totals
+  // (2 block barriers instead of the 2 log2(kScanS) of a Hillis-Steele scan over the block)
+  static_assert(kScanP * kScanS == 1024 && 32 % kScanP == 0 && kScanP <= 32, "scan shape");
+  const int wl = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto shfl_up_map = [](const AffMap& x, int o) {
+    return AffMap{__shfl_up_sync(kFull, x.E, o), __shfl_up_sync(kFull, x.L, o),
+                  __shfl_up_sync(kFull, x.Sb, o), __shfl_up_sync(kFull, x.Qb, o)};
+  };
+#pragma unroll
+  for (int o = kScanP; o < 32; o <<= 1) {
+    const AffMap up = shfl_up_map(m, o);
+    if (wl >= o) m = compose(up, m);
   }
+  if (wl >= 32 - kScanP) sm[wid][lane] = m;     // this warp's total (its last segment), per pair
+  __syncthreads();
+  if (wid < kScanP) {                           // warp q scans the 32 warp totals of pair q
+    AffMap t = sm[wl][wid];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const AffMap up = shfl_up_map(t, o);
+      if (wl >= o) t = compose(up, t);
+    }
+    sm[wl][wid] = t;
+  }
+  __syncthreads();
+  if (wid > 0) m = compose(sm[wid - 1][lane], m);   // inclusive map through this segment
+  // inclusive map through the previous segment (the second walk's starting point)
+  const AffMap up1 = shfl_up_map(m, kScanP);
+  const AffMap prevm = wl >= kScanP ? up1 : (wid > 0 ? sm[wid - 1][lane] : AffMap{1.0f, 0.0f, 0.0f, 0.0f});
   if (!valid) return;
   // state carried into this slice (f1, multi-GPU): the earlier slices' maps composed in order
   float2 x0 = make_float2(0.0f, 0.0f);
@@ -477,7 +497,7 @@ k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __res
   }
   if (maps_only) return;
   // state entering segment seg = (inclusive map of segment seg-1) applied to the carried state
-  float2 x = seg > 0 ? apply(sm[seg - 1][lane], x0) : x0;
+  float2 x = seg > 0 ? apply(prevm, x0) : x0;
   for (int64_t c = c0; c < c1; c += kScanB) {
     float Lb[kScanB];
     float2 lb[kScanB];
