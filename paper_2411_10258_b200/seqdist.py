@@ -57,6 +57,8 @@ def make_slice(D, t_slice, m_slice, T, t0, rank, chunk_events=256, cfg: FitConfi
 class LocalComm:
     """All R ranks live in this process: collectives are stacks and sums of the per-rank lists."""
 
+    graph_safe = True
+
     def __init__(self, R):
         self.R = R
 
@@ -75,6 +77,8 @@ class TorchComm:
         self.dist = dist
         self.group = group
         self.R = dist.get_world_size(group)
+        # NCCL collectives can be captured in CUDA graphs; gloo ones cannot
+        self.graph_safe = dist.get_backend(group) == "nccl"
 
     def all_gather(self, xs):
         (x,) = xs
@@ -105,28 +109,38 @@ def _stats(ctxs, comm, stream=None):
 
 
 def _parts(ctxs, comm, theta, alpha, beta, grad, fit, stream=None):
-    """One distributed evaluation: maps -> all_gather -> parts -> all_reduce.  Returns
-    (reduced parts, global final state).  theta/alpha/beta are per-context lists (identical)."""
+    """One distributed evaluation: maps -> all_gather -> parts -> all_reduce (two collectives).
+    Returns (reduced parts, global final state).  theta/alpha/beta are per-context lists
+    (identical).  The final state (the last slice's) rides in the all-reduce: every other rank
+    contributes exact zeros, so the sum is that state bit for bit."""
     D = ctxs[0].D
-    maps, spans = [], []
+    DD = D * D
+    R = comm.R
+    bufs = []
     for c, be in zip(ctxs, beta):
-        mp = torch.empty(D * D, 2, dtype=torch.float32, device=c.work.device)
-        sp = torch.empty(1, dtype=torch.float32, device=c.work.device)
-        _check(lib().mdhp_seq_maps(ctypes.byref(c.ps.desc), _ptr(c.ps.buf), _ptr(be), _ptr(c.work), _ptr(mp),
-                                   _ptr(sp), int(fit), _stream(stream)), "mdhp_seq_maps")
-        maps.append(mp); spans.append(sp)
-    M = comm.all_gather(maps).contiguous()            # [R, D*D, 2]
-    Sp = comm.all_gather(spans).reshape(-1).contiguous()
-    parts, fins = [], []
+        mb = torch.empty(2 * DD + 1, dtype=torch.float32, device=c.work.device)   # [maps | span]
+        _check(lib().mdhp_seq_maps(ctypes.byref(c.ps.desc), _ptr(c.ps.buf), _ptr(be), _ptr(c.work), _ptr(mb),
+                                   _ptr(mb[2 * DD:]), int(fit), _stream(stream)), "mdhp_seq_maps")
+        bufs.append(mb)
+    G = comm.all_gather(bufs)                          # [R, 2 D^2 + 1]
+    M = G[:, :2 * DD].contiguous()                     # [R][D*D] float2
+    Sp = G[:, 2 * DD].contiguous()                     # [R]
+    NP = 2 * DD + D + 1
+    red = []
     for c, th, al, be in zip(ctxs, theta, alpha, beta):
-        pt = torch.empty(2 * D * D + D + 1, dtype=torch.float64, device=c.work.device)
-        fn = torch.empty(D * D, 2, dtype=torch.float32, device=c.work.device)
+        pb = torch.empty(NP + 2 * DD, dtype=torch.float64, device=c.work.device)   # [parts | final state]
+        fn = torch.empty(DD, 2, dtype=torch.float32, device=c.work.device)
         _check(lib().mdhp_seq_parts(ctypes.byref(c.ps.desc), _ptr(c.ps.buf), _ptr(th), _ptr(al), _ptr(be), _ptr(M),
-                                    _ptr(Sp), c.rank, _ptr(c.work), _ptr(pt), _ptr(fn), int(grad), int(fit),
+                                    _ptr(Sp), c.rank, _ptr(c.work), _ptr(pb), _ptr(fn), int(grad), int(fit),
                                     _stream(stream)), "mdhp_seq_parts")
-        parts.append(pt); fins.append(fn)
-    P = comm.all_reduce_sum(parts)
-    F = comm.all_gather(fins)[-1].contiguous()         # the last slice ends the sequence
+        if c.rank == R - 1:
+            pb[NP:].copy_(fn.reshape(-1))
+        else:
+            pb[NP:].zero_()
+        red.append(pb)
+    S = comm.all_reduce_sum(red)
+    P = S[:NP].contiguous()
+    F = S[NP:].to(torch.float32).reshape(DD, 2).contiguous()
     return P, F
 
 
@@ -150,10 +164,12 @@ def loglik_grad(ctxs, comm, theta, alpha, beta, n_total, grads=True, stream=None
     return {"lnl": lnl, "g_theta": gt, "g_alpha": ga, "g_beta": gb}
 
 
-def fit(ctxs, comm, params, cfg: FitConfig, n_total, stream=None):
+def fit(ctxs, comm, params, cfg: FitConfig, n_total, stream=None, graph=None):
     """Distributed fit of one sequence: the DESIGN.md "Fit" loop with one exchange pair per
     iteration.  params: per-local-context dicts of CUDA tensors theta [D], alpha/beta [D,D]
-    (updated in place, identical on all ranks).  ctxs must have been made with cfg."""
+    (updated in place, identical on all ranks).  ctxs must have been made with cfg.
+    graph (default: when the comm is graph-safe and no explicit stream is given): replay one
+    captured iteration (kernels + collectives) as a CUDA graph."""
     stats = _stats(ctxs, comm, stream)
     c = cfg.c()
     outs = []
@@ -163,8 +179,8 @@ def fit(ctxs, comm, params, cfg: FitConfig, n_total, stream=None):
                      "iters": torch.zeros(1, dtype=torch.int32, device=dev),
                      "status": torch.zeros(1, dtype=torch.int32, device=dev)})
     th = [p["theta"] for p in params]; al = [p["alpha"] for p in params]; be = [p["beta"] for p in params]
-    for it in range(cfg.max_iters + 1):
-        final = it == cfg.max_iters
+
+    def iteration(final):
         P, F = _parts(ctxs, comm, th, al, be, grad=0 if final else 1, fit=0 if final else 1, stream=stream)
         for x, p, o in zip(ctxs, params, outs):
             _check(lib().mdhp_seq_finish(ctypes.byref(x.ps.desc), int(n_total), _ptr(stats), _ptr(P), _ptr(F),
@@ -172,4 +188,25 @@ def fit(ctxs, comm, params, cfg: FitConfig, n_total, stream=None):
                                          None, None, ctypes.byref(c), _ptr(x.work), None, None, _ptr(o["status"]),
                                          _ptr(o["iters"]), int(final), _ptr(x.ps.buf), _stream(stream)),
                    "mdhp_seq_finish")
+
+    if graph is None:
+        graph = stream is None and getattr(comm, "graph_safe", False)
+    if graph and cfg.max_iters > 1:
+        # iteration 0 runs eagerly (it also initialises the communicator), the rest replay one
+        # captured iteration: kernels and collectives, no host round trip; the device-side control
+        # block stops the updates once the loop is done (as in mdhp_seq_fit)
+        iteration(False)
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                iteration(False)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        for _ in range(cfg.max_iters - 1):
+            g.replay()
+        iteration(True)
+    else:
+        for it in range(cfg.max_iters + 1):
+            iteration(it == cfg.max_iters)
     return outs

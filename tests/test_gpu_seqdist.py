@@ -83,3 +83,60 @@ def test_dist_fit_matches_single(opt):
         np.testing.assert_allclose(p["theta"].cpu().numpy(), th.cpu().numpy(), rtol=1e-4, atol=1e-6)
     assert int(outs[0]["iters"][0]) == int(r["iters"][0]) == 20
     assert float(outs[0]["lnl"][0]) == pytest.approx(float(r["lnl"][0]), rel=1e-6)
+
+
+def _fit_once(D, t, m, T, R, cfg, comm, graph, init):
+    ctxs = _slices(D, t, m, T, R, cfg=cfg)
+    params = [{"theta": torch.tensor(init[0], device=DEV), "alpha": torch.tensor(init[1], device=DEV),
+               "beta": torch.tensor(init[2], device=DEV)} for _ in range(R)]
+    outs = seqdist.fit(ctxs, comm, params, cfg, n_total=len(t), graph=graph)
+    torch.cuda.synchronize()
+    return params, outs
+
+
+def test_dist_fit_graph_replay_equals_eager():
+    """The distributed fit replayed as one captured CUDA graph per iteration (kernels and the two
+    exchanges) gives bit-identical parameters, lnL and iteration counts to the eager loop."""
+    D, T, R = 4, 30.0, 3
+    t, m, _ = seq_case(D, T, 30.0, seed=41)
+    cfg = M.FitConfig(max_iters=25, optimizer="adam", lr=0.05, tol_rel=0.0)
+    init = (np.full(D, 2.0, np.float32), np.full((D, D), 0.5, np.float32), np.full((D, D), 2.0, np.float32))
+    pe, oe = _fit_once(D, t, m, T, R, cfg, seqdist.LocalComm(R), False, init)
+    pg, og = _fit_once(D, t, m, T, R, cfg, seqdist.LocalComm(R), True, init)
+    for a, b in zip(pe, pg):
+        for k in ("theta", "alpha", "beta"):
+            np.testing.assert_array_equal(a[k].cpu().numpy(), b[k].cpu().numpy())
+    assert float(oe[0]["lnl"][0]) == float(og[0]["lnl"][0])
+    assert int(oe[0]["iters"][0]) == int(og[0]["iters"][0]) == 25
+
+
+def test_dist_fit_nccl_single_rank_graph():
+    """TorchComm over a real NCCL process group (world size 1 on this GPU): the collectives are
+    captured in the iteration graph; the result equals the single-GPU sequence fit."""
+    import os
+    import socket
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        D, T = 3, 30.0
+        t, m, _ = seq_case(D, T, 30.0, seed=43)
+        cfg = M.FitConfig(max_iters=20, optimizer="adam", lr=0.05, tol_rel=0.0)
+        init = (np.full(D, 2.0, np.float32), np.full((D, D), 0.5, np.float32), np.full((D, D), 2.0, np.float32))
+        comm = seqdist.TorchComm()
+        assert comm.graph_safe
+        pg, og = _fit_once(D, t, m, T, 1, cfg, comm, None, init)
+        ps = M.seq_pack(D, torch.tensor(t, device=DEV), torch.tensor(m, dtype=torch.int32, device=DEV), T,
+                        chunk_events=32)
+        th, al, be = (torch.tensor(x, device=DEV) for x in init)
+        r = M.seq_fit(ps, th, al, be, cfg)
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(pg[0]["alpha"].cpu().numpy(), al.cpu().numpy(), rtol=1e-4, atol=1e-6)
+        np.testing.assert_allclose(pg[0]["beta"].cpu().numpy(), be.cpu().numpy(), rtol=1e-4, atol=1e-6)
+        assert int(og[0]["iters"][0]) == 20
+        assert float(og[0]["lnl"][0]) == pytest.approx(float(r["lnl"][0]), rel=1e-6)
+    finally:
+        dist.destroy_process_group()
