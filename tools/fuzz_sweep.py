@@ -59,5 +59,47 @@ def main(n):
     return 0 if worst_r17 <= 1.0 and worst_g <= 1.0 else 1
 
 
+
+
+def fit_sweep(n, iters=5):
+    """Random-start Adam fits (lr 0.02, `iters` iterations) vs the oracle's: parameters within
+    R17 (1e-3 relative, floor 1e-2 of the group mean); prints the worst ratio to that bar."""
+    worst, windows = 0.0, 0
+    for k in range(n):
+        rng = np.random.default_rng(70000 + k)
+        D = int(rng.integers(1, 33))
+        W = int(rng.integers(1, 16))
+        b = fuzz_windows(rng, D, W)
+        th, al, be = fuzz_params(rng, W, D)
+        be = np.clip(be, 0.05, None)
+        dev = (torch.tensor(b["t"], dtype=torch.float64, device="cuda"),
+               torch.tensor(b["mark"], dtype=torch.int32, device="cuda"),
+               torch.tensor(b["win_off"], dtype=torch.int64, device="cuda"),
+               torch.tensor(b["T"], dtype=torch.float64, device="cuda"))
+        pk = M.pack_windows(D, *dev)
+        tt = [torch.tensor(f32(x), device="cuda") for x in (th, al, be)]
+        M.fit(pk, *tt, M.FitConfig(max_iters=iters, optimizer="adam", lr=0.02, tol_rel=0.0))
+        g = [x.cpu().numpy() for x in tt]
+        t32, T32, _ = H.oracle_times(b, D)
+        ocfg = oracle.FitConfig(max_iters=iters, optimizer="adam", lr=0.02, tol_rel=0.0)
+        for w in range(W):
+            a, z = b["win_off"][w], b["win_off"][w + 1]
+            o = oracle.fit(D, t32[a:z], b["mark"][a:z], T32[w], f32(th[w]).astype(float),
+                           f32(al[w]).astype(float), f32(be[w]).astype(float), ocfg)
+            for got, key in zip(g, ("theta", "alpha", "beta")):
+                ref = o[key]
+                s = 1e-2 * max(np.mean(np.abs(ref)), 1e-4)
+                r = float(np.max(np.abs(got[w] - ref) / (1e-3 * np.maximum(np.abs(ref), s))))
+                if r > 1:
+                    print(f"  fit out of bar: batch {k} D={D} window {w} n={z - a} {key} ratio {r:.3g}", flush=True)
+                worst = max(worst, r)
+            windows += 1
+    print(f"fit sweep: {n} batches, {windows} windows, {iters} Adam iterations: worst parameter error "
+          f"{worst:.3g} x the R17 tolerance (bar 1)")
+    return 0 if worst <= 1 else 1
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "fit":
+        sys.exit(fit_sweep(int(sys.argv[2]) if len(sys.argv) > 2 else 200))
     sys.exit(main(int(sys.argv[1]) if len(sys.argv) > 1 else 300))
