@@ -275,6 +275,47 @@ def bench_seq(args, rc, world, rank, dev):
     return 0
 
 
+def run_e2e(M, b, D, W, cfg, init_th, init_al, init_be, ev_it_per_step, world, dev):
+    """e2e: the same metric through mdhp_fit_host on pinned host buffers (H2D of the CSR and the
+    init, pack, fit, D2H of the results inside the timed call), after one untimed warm-up call.
+    If a rank cannot pin its host buffers (host memory at N = 8), every rank reports the reason
+    instead of the number (agreed by an all-reduce, so no rank waits in a barrier alone)."""
+    import torch
+    import torch.distributed as dist
+    err = None
+    try:
+        t_h = b["t"].cpu().pin_memory(); m_h = b["mark"].cpu().pin_memory()
+        o_h = b["win_off"].cpu().pin_memory(); T_h = b["T"].cpu().pin_memory()
+        th_h = init_th.cpu().pin_memory(); al_h = init_al.cpu().pin_memory(); be_h = init_be.cpu().pin_memory()
+        ths, als, bes = th_h.clone().pin_memory(), al_h.clone().pin_memory(), be_h.clone().pin_memory()
+    except (RuntimeError, MemoryError) as ex:
+        err = f"{type(ex).__name__}: {str(ex)[:200]}"
+    ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=dev)
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if int(ok[0]) == 0:
+        return {"value": None, "unit": UNIT, "error": err or "another rank could not pin its host buffers"}
+    bi = sum(x.numel() * x.element_size() for x in (t_h, m_h, o_h, T_h, th_h, al_h, be_h))
+    bo = (th_h.numel() + al_h.numel() + be_h.numel()) * 4 + W * (8 + 4 + 4)
+    ke = 1   # one untimed warm-up call (workspace pool), then ke timed calls
+    M.fit_host(D, t_h, m_h, o_h, T_h, ths, als, bes, cfg, time_mode=1)
+    dt = 0.0
+    for _ in range(ke):
+        ths.copy_(th_h); als.copy_(al_h); bes.copy_(be_h)   # reset the init (host, untimed)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        M.fit_host(D, t_h, m_h, o_h, T_h, ths, als, bes, cfg, time_mode=1)
+        dt += time.perf_counter() - t0
+    dt /= ke
+    dtt = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(dtt, op=dist.ReduceOp.MAX)
+    return {"value": ev_it_per_step / float(dtt), "unit": UNIT,
+            "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo), "steps": ke,
+            "api": "mdhp_fit_host (pinned host CSR in, fitted params/lnL/iters/status out)"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
 
@@ -513,29 +554,7 @@ def main():
     # ---- end to end through the public C ABI on HOST buffers (mdhp_fit_host), copies inside
     e2e = None
     if not args.no_e2e:
-        t_h = b["t"].cpu().pin_memory(); m_h = b["mark"].cpu().pin_memory()
-        o_h = b["win_off"].cpu().pin_memory(); T_h = b["T"].cpu().pin_memory()
-        th_h = init_th.cpu().pin_memory(); al_h = init_al.cpu().pin_memory(); be_h = init_be.cpu().pin_memory()
-        bi = sum(x.numel() * x.element_size() for x in (t_h, m_h, o_h, T_h, th_h, al_h, be_h))
-        bo = (th_h.numel() + al_h.numel() + be_h.numel()) * 4 + W * (8 + 4 + 4)
-        ths, als, bes = th_h.clone().pin_memory(), al_h.clone().pin_memory(), be_h.clone().pin_memory()
-        ke = 1   # one untimed warm-up call (workspace pool), then ke timed calls
-        M.fit_host(D, t_h, m_h, o_h, T_h, ths, als, bes, cfg, time_mode=1)
-        dt = 0.0
-        for _ in range(ke):
-            ths.copy_(th_h); als.copy_(al_h); bes.copy_(be_h)   # reset the init (host, untimed)
-            if world > 1:
-                dist.barrier()
-            t0 = time.perf_counter()
-            M.fit_host(D, t_h, m_h, o_h, T_h, ths, als, bes, cfg, time_mode=1)
-            dt += time.perf_counter() - t0
-        dt /= ke
-        dtt = torch.tensor([dt], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(dtt, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(tot[0]) / args.steps / float(dtt), "unit": UNIT,
-               "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo), "steps": ke,
-               "api": "mdhp_fit_host (pinned host CSR in, fitted params/lnL/iters/status out)"}
+        e2e = run_e2e(M, b, D, W, cfg, init_th, init_al, init_be, float(tot[0]) / args.steps, world, dev)
 
     # ---- roofline of the dominant kernel (k_fit): algorithmic MUFU ops / its CUDA-event time
     mufu_per_ev = 2 * D + 2
