@@ -250,6 +250,12 @@ k_seq_momsum(int Dp, int64_t C, const float* __restrict__ cmom, float* __restric
 }
 
 // ---------------------------------------------------------------- evaluation workspace
+#ifndef MDHP_SCAN_P
+#define MDHP_SCAN_P 4
+#endif
+constexpr int kScanP = MDHP_SCAN_P, kScanS = 1024 / MDHP_SCAN_P;   // pairs x segments per scan
+                                                                  // block (1024 threads)
+
 // Phase-3 blocks: 4 warps x G chunks each; every block writes one record of partial sums.
 inline int64_t seq_eval_blocks(int Dp, int64_t C) {
   const int64_t per = 4 * (32 / Dp);
@@ -267,6 +273,7 @@ struct SeqWork {
   float* prev;     // [D + 2 D^2] previous point (rollback)
   float* opt;      // [2 (D + 2 D^2)] Adam moments when the caller passes none
   double* rpart;   // [phase-3 blocks][2 D^2 + D + 1] per-block partial sums
+  float4* segmap;  // [D*D][kScanS + 1] scan segment maps kept between mdhp_seq_maps and _parts (f1)
   size_t bytes;
 };
 
@@ -279,7 +286,8 @@ inline SeqWork make_seq_work(void* base, int D, int Dp, int64_t C) {
                f = take(sizeof(float2) * DD), gs = take(sizeof(float2) * DD),
                gt = take(sizeof(float) * Dp), ls = take(sizeof(double)),
                ct = take(sizeof(int) * 64), pv = take(sizeof(float) * P), op = take(sizeof(float) * 2 * P),
-               rp = take(sizeof(double) * (size_t)seq_eval_blocks(Dp, C) * (2 * DD + D + 1));
+               rp = take(sizeof(double) * (size_t)seq_eval_blocks(Dp, C) * (2 * DD + D + 1)),
+               sg = take(sizeof(float4) * DD * (kScanS + 1));
   char* B = static_cast<char*>(base);
   w.loc = reinterpret_cast<float2*>(B + a);
   w.carry = reinterpret_cast<float2*>(B + b);
@@ -291,6 +299,7 @@ inline SeqWork make_seq_work(void* base, int D, int Dp, int64_t C) {
   w.prev = reinterpret_cast<float*>(B + pv);
   w.opt = reinterpret_cast<float*>(B + op);
   w.rpart = reinterpret_cast<double*>(B + rp);
+  w.segmap = reinterpret_cast<float4*>(B + sg);
   w.bytes = o;
   return w;
 }
@@ -402,11 +411,6 @@ __device__ __forceinline__ AffMap compose(const AffMap& m1, const AffMap& m2) {
   return r;
 }
 
-#ifndef MDHP_SCAN_P
-#define MDHP_SCAN_P 4
-#endif
-constexpr int kScanP = MDHP_SCAN_P, kScanS = 1024 / MDHP_SCAN_P;   // pairs x segments per scan
-                                                                  // block (1024 threads)
 constexpr int kScanB = 4;                  // chunks per load batch of a segment walk
 
 __global__ void __launch_bounds__(kScanP * kScanS)
@@ -414,7 +418,10 @@ k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __res
            const float2* __restrict__ loc, float2* __restrict__ carry, float2* __restrict__ fin,
            const int* __restrict__ ctl, const float2* __restrict__ maps,
            const float* __restrict__ spans, int rank, float2* __restrict__ rankmap,
-           float* __restrict__ rankspan, int maps_only) {
+           float* __restrict__ rankspan, int mode, float4* __restrict__ segmap) {
+  // mode 0: whole scan; 1 (f1 mdhp_seq_maps): slice map only, the segment maps kept in segmap;
+  // 2 (f1 mdhp_seq_parts, same beta and local states): the kept segment maps replace the first
+  // walk and the block scan, only the carried states are written
   if (ctl && ctl[0]) return;
   __shared__ AffMap sm[32][kScanP];   // per-warp totals (32 warps of 1024 threads)
   const int lane = threadIdx.x % kScanP, seg = threadIdx.x / kScanP;
@@ -424,58 +431,74 @@ k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __res
   const float b = valid ? beta[p] : 0.0f;
   const int64_t per = (C + kScanS - 1) / kScanS;
   const int64_t c0 = min(C, (int64_t)seg * per), c1 = min(C, c0 + per);
-  // segment walks in batches of kScanB chunks: all loads of a batch are issued before the
-  // (sequential) compose chain uses them, instead of one L2 round trip per chunk
-  AffMap m{1.0f, 0.0f, 0.0f, 0.0f};
-  if (valid) {
-    for (int64_t c = c0; c < c1; c += kScanB) {
-      float Lb[kScanB];
-      float2 lb[kScanB];
-#pragma unroll
-      for (int k = 0; k < kScanB; k++) {
-        const bool in = c + k < c1;
-        Lb[k] = in ? cspan[c + k] : 0.0f;
-        lb[k] = in ? loc[(c + k) * DD + p] : make_float2(0.0f, 0.0f);
+  AffMap m{1.0f, 0.0f, 0.0f, 0.0f}, prevm{1.0f, 0.0f, 0.0f, 0.0f};
+  const size_t sgb = (size_t)p * (kScanS + 1);
+  if (mode == 2) {
+    if (valid) {
+      const float4 a = segmap[sgb + seg];
+      prevm = AffMap{a.x, a.y, a.z, a.w};
+      if (seg == kScanS - 1) {
+        const float4 t = segmap[sgb + kScanS];
+        m = AffMap{t.x, t.y, t.z, t.w};
       }
+    }
+  } else {
+    // segment walks in batches of kScanB chunks: all loads of a batch are issued before the
+    // (sequential) compose chain uses them, instead of one L2 round trip per chunk
+    if (valid) {
+      for (int64_t c = c0; c < c1; c += kScanB) {
+        float Lb[kScanB];
+        float2 lb[kScanB];
 #pragma unroll
-      for (int k = 0; k < kScanB; k++) {
-        if (c + k < c1) {
-          const AffMap mc{ex2f(b * (Lb[k] * -kLog2e)), Lb[k], lb[k].x, lb[k].y};
-          m = compose(m, mc);
+        for (int k = 0; k < kScanB; k++) {
+          const bool in = c + k < c1;
+          Lb[k] = in ? cspan[c + k] : 0.0f;
+          lb[k] = in ? loc[(c + k) * DD + p] : make_float2(0.0f, 0.0f);
+        }
+#pragma unroll
+        for (int k = 0; k < kScanB; k++) {
+          if (c + k < c1) {
+            const AffMap mc{ex2f(b * (Lb[k] * -kLog2e)), Lb[k], lb[k].x, lb[k].y};
+            m = compose(m, mc);
+          }
         }
       }
     }
-  }
-  // inclusive scan of the segment maps (per pair, over segments) in two levels: shuffles
-  // within each warp (32 / kScanP segments), then one warp per pair scans the 32 warp totals
-  // (2 block barriers instead of the 2 log2(kScanS) of a Hillis-Steele scan over the block)
-  static_assert(kScanP * kScanS == 1024 && 32 % kScanP == 0 && kScanP <= 32, "scan shape");
-  const int wl = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  auto shfl_up_map = [](const AffMap& x, int o) {
-    return AffMap{__shfl_up_sync(kFull, x.E, o), __shfl_up_sync(kFull, x.L, o),
-                  __shfl_up_sync(kFull, x.Sb, o), __shfl_up_sync(kFull, x.Qb, o)};
-  };
+    // inclusive scan of the segment maps (per pair, over segments) in two levels: shuffles
+    // within each warp (32 / kScanP segments), then one warp per pair scans the 32 warp totals
+    // (2 block barriers instead of the 2 log2(kScanS) of a Hillis-Steele scan over the block)
+    static_assert(kScanP * kScanS == 1024 && 32 % kScanP == 0 && kScanP <= 32, "scan shape");
+    const int wl = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    auto shfl_up_map = [](const AffMap& x, int o) {
+      return AffMap{__shfl_up_sync(kFull, x.E, o), __shfl_up_sync(kFull, x.L, o),
+                    __shfl_up_sync(kFull, x.Sb, o), __shfl_up_sync(kFull, x.Qb, o)};
+    };
 #pragma unroll
-  for (int o = kScanP; o < 32; o <<= 1) {
-    const AffMap up = shfl_up_map(m, o);
-    if (wl >= o) m = compose(up, m);
-  }
-  if (wl >= 32 - kScanP) sm[wid][lane] = m;     // this warp's total (its last segment), per pair
-  __syncthreads();
-  if (wid < kScanP) {                           // warp q scans the 32 warp totals of pair q
-    AffMap t = sm[wl][wid];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const AffMap up = shfl_up_map(t, o);
-      if (wl >= o) t = compose(up, t);
+    for (int o = kScanP; o < 32; o <<= 1) {
+      const AffMap up = shfl_up_map(m, o);
+      if (wl >= o) m = compose(up, m);
     }
-    sm[wl][wid] = t;
+    if (wl >= 32 - kScanP) sm[wid][lane] = m;     // this warp's total (its last segment), per pair
+    __syncthreads();
+    if (wid < kScanP) {                           // warp q scans the 32 warp totals of pair q
+      AffMap t = sm[wl][wid];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const AffMap up = shfl_up_map(t, o);
+        if (wl >= o) t = compose(up, t);
+      }
+      sm[wl][wid] = t;
+    }
+    __syncthreads();
+    if (wid > 0) m = compose(sm[wid - 1][lane], m);   // inclusive map through this segment
+    // inclusive map through the previous segment (the second walk's starting point)
+    const AffMap up1 = shfl_up_map(m, kScanP);
+    prevm = wl >= kScanP ? up1 : (wid > 0 ? sm[wid - 1][lane] : AffMap{1.0f, 0.0f, 0.0f, 0.0f});
+    if (mode == 1 && valid && segmap) {
+      segmap[sgb + seg] = make_float4(prevm.E, prevm.L, prevm.Sb, prevm.Qb);
+      if (seg == kScanS - 1) segmap[sgb + kScanS] = make_float4(m.E, m.L, m.Sb, m.Qb);
+    }
   }
-  __syncthreads();
-  if (wid > 0) m = compose(sm[wid - 1][lane], m);   // inclusive map through this segment
-  // inclusive map through the previous segment (the second walk's starting point)
-  const AffMap up1 = shfl_up_map(m, kScanP);
-  const AffMap prevm = wl >= kScanP ? up1 : (wid > 0 ? sm[wid - 1][lane] : AffMap{1.0f, 0.0f, 0.0f, 0.0f});
   if (!valid) return;
   // state carried into this slice (f1, multi-GPU): the earlier slices' maps composed in order
   float2 x0 = make_float2(0.0f, 0.0f);
@@ -495,7 +518,7 @@ k_seq_scan(int D, int64_t C, const float* __restrict__ cspan, const float* __res
     if (rankmap) rankmap[p] = make_float2(m.Sb, m.Qb);
     if (rankspan && p == 0) rankspan[0] = m.L;
   }
-  if (maps_only) return;
+  if (mode == 1) return;
   // state entering segment seg = (inclusive map of segment seg-1) applied to the carried state
   float2 x = seg > 0 ? apply(prevm, x0) : x0;
   for (int64_t c = c0; c < c1; c += kScanB) {
@@ -884,7 +907,7 @@ struct SeqDist {   // multi-GPU slice context (f1); all null/zero for a whole se
   float2* rankmap = nullptr;
   float* rankspan = nullptr;
   int maps_only = 0;
-  int skip_local = 0;
+  int skip_local = 0;   // mdhp_seq_parts after mdhp_seq_maps: local states and scan segment maps reused
 };
 
 template <int DP>
@@ -905,7 +928,8 @@ static void seq_phases_t(const SeqLayout& L, const void* pk, const float* th, co
   }
   k_seq_scan<<<(L.D * L.D + kScanP - 1) / kScanP, kScanP * kScanS, 0, st>>>(L.D, C, at<float>(pk, L.cspan), be, w.loc, w.carry,
                                              w.fin, grad ? ctl : nullptr, sd.maps, sd.spans,
-                                             sd.rank, sd.rankmap, sd.rankspan, sd.maps_only);
+                                             sd.rank, sd.rankmap, sd.rankspan,
+                                             sd.maps_only ? 1 : (sd.skip_local ? 2 : 0), w.segmap);
   count_launch();
   if (sd.maps_only) return;
   const int has_history = sd.has_history;
@@ -1203,12 +1227,13 @@ static SeqFinishArea finish_area(void* work, int Dp) {
 size_t seq_work_bytes_slice(int D, int64_t N, int ce) {
   const SeqLayout L = make_seq_layout(D, N, ce);
   const size_t wb = make_seq_work(nullptr, D, L.Dp, L.C).bytes;
-  return wb + 8192 + sizeof(float2) * (size_t)D * D;   // + the head region of finish_area
+  return wb + align256(8192 + sizeof(float2) * (size_t)D * D);   // + the head region of finish_area
 }
 
 static SeqWork slice_work(int D, int64_t N, int ce, void* work) {
   const SeqLayout L = make_seq_layout(D, N, ce);
-  char* base = static_cast<char*>(work) + 8192 + sizeof(float2) * (size_t)D * D;   // after the head
+  // after the head, 256-byte aligned (the work arrays include float4 segment maps)
+  char* base = static_cast<char*>(work) + align256(8192 + sizeof(float2) * (size_t)D * D);
   return make_seq_work(base, D, L.Dp, L.C);
 }
 
@@ -1256,7 +1281,7 @@ int seq_parts_launch(int D, int64_t N, int ce, const void* pk, const float* th, 
     cudaMemsetAsync(parts, 0, sizeof(double) * (2 * DD + D + 1), st);
     k_seq_scan<<<(D * D + kScanP - 1) / kScanP, kScanP * kScanS, 0, st>>>(D, 0, nullptr, be, nullptr, nullptr, fin,
                                                           nullptr, maps, spans, rank, nullptr,
-                                                          nullptr, 1);
+                                                          nullptr, 1, nullptr);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? MDHP_OK : MDHP_ECUDA;
   }

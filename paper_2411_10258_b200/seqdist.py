@@ -196,12 +196,18 @@ def fit(ctxs, comm, params, cfg: FitConfig, n_total, stream=None, graph=None):
         # captured iteration: kernels and collectives, no host round trip; the device-side control
         # block stops the updates once the loop is done (as in mdhp_seq_fit)
         iteration(False)
+        # capture_begin/end directly: the torch.cuda.graph context manager also runs gc.collect()
+        # and empties the allocator cache on entry (tens of ms, and every later allocation pays
+        # cudaMalloc again), which made a fit's wall time vary 4x from call to call
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):
-            with torch.cuda.graph(g, stream=side):
+            g.capture_begin()
+            try:
                 iteration(False)
+            finally:
+                g.capture_end()
         torch.cuda.current_stream(dev).wait_stream(side)
         for _ in range(cfg.max_iters - 1):
             g.replay()
