@@ -189,7 +189,7 @@ def bench_seq_sharded(args, rc, world, rank, dev):
                                  rank, chunk_events=args.chunk, cfg=cfg)
         p = {"theta": th0.clone(), "alpha": al0.clone(), "beta": be0.clone()}
         return seqdist.fit([ctx], comm, [p], cfg, n_total=N)[0]
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 1)):
         o = step()
     torch.cuda.synchronize()
     evals = int(o["iters"][0]) + 1
@@ -243,7 +243,7 @@ def bench_seq(args, rc, world, rank, dev):
         th.copy_(th0); al.copy_(al0); be.copy_(be0)
         M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=ce, out=ps)
         return M.seq_fit(ps, th, al, be, cfg)
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 1)):
         r = step()
     torch.cuda.synchronize()
     evals = int(r["iters"][0]) + 1
@@ -512,7 +512,7 @@ def main():
             shard.gather_records(rec, world, rank, out=gathered)
         return r
 
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 1)):   # at least one: the iteration counts come from it
         r = step()
     torch.cuda.synchronize()
     iters_run = r["iters"].to(torch.int64)
