@@ -585,8 +585,9 @@ def main():
     if Dp == 16:
         # the same pipe measured by ncu on this kernel (all shared wavefronts incl. the
         # non-loop phases, plus SHFL), not the algorithmic count above
-        mio["ncu_measured_frac"] = 0.803
-        mio["ncu_source"] = "profiles/r01_k_fit_v10_wavefronts.txt (16,384 windows x 101 evaluations)"
+        mio["ncu_measured_frac"] = 0.848
+        mio["ncu_source"] = ("profiles/r01_k_fit_fullsize_mio.txt (this launch configuration: shared "
+                             "wavefronts 79.1% + SHFL 5.7% of all SM cycles)")
     roof = {"bound": "alu", "achieved": achieved, "peak": MUFU_PEAK_GOPS, "unit": "Gop/s (MUFU)",
             "frac": achieved / MUFU_PEAK_GOPS, "traffic": traffic, "kernel": f"k_fit<{Dp}>",
             "per_unit": f"{mufu_per_ev} MUFU ops per event-iteration (2D ex2 + lg2 + rcp)",
