@@ -203,7 +203,11 @@ int mdhp_fit(const mdhp_pack_desc* desc, const void* packed, const mdhp_fit_conf
  * mdhp_fit_host — end-to-end convenience call on HOST buffers (pinned memory recommended):
  * copies the CSR batch and initial parameters to the device, packs, fits, and copies the
  * fitted parameters, loglik, iters and status back.  Same arguments as pack + fit with host
- * pointers.  Synchronous (returns after the device->host copies completed).
+ * pointers (win_off_host[0] must be 0 and win_off_host[W] = n_events, else MDHP_EINVAL).
+ * Synchronous (returns after the device->host copies completed).  From 4,096 windows on, the
+ * batch is processed as 4 window ranges: the uploads run on a private copy stream and overlap
+ * the fits on `stream`, each range's results go back while the next range fits (windows are
+ * independent: the outputs equal those of pack + fit on the whole batch).
  * Workspace comes from the device's default stream-ordered memory pool; mdhp_fit and
  * mdhp_fit_host raise that pool's release threshold (once per device) so repeated calls reuse
  * the memory instead of re-mapping it (cudaMemPoolTrimTo releases it).

@@ -49,6 +49,7 @@ int seq_fit_launch(int D, int64_t N, int ce, double T, const void* pk, const Fit
                    int32_t* status, float* trace, cudaStream_t st);
 size_t seq_packed_bytes(int D, int64_t N, int ce);
 int seq_chunk_hint(int D, int64_t N);
+void rebase_offsets_launch(int64_t* off, int64_t n, int64_t base, cudaStream_t st);
 
 static thread_local char g_err[512] = "";
 static std::atomic<uint64_t> g_launches{0};
@@ -524,29 +525,45 @@ int mdhp_fit_host(const mdhp_pack_desc* d, const double* t_h, const int32_t* mar
     set_error("NULL pointer argument");
     return MDHP_EINVAL;
   }
-  cudaStream_t st = (cudaStream_t)stream;
+  if (off_h[0] != 0 || off_h[d->n_windows] != d->n_events) {
+    set_error("win_off must run from 0 to n_events");
+    return MDHP_EINVAL;
+  }
+  cudaStream_t cs = (cudaStream_t)stream;
   keep_pool_memory();
   const int64_t W = d->n_windows, E = d->n_events;
   const int D = d->D;
-  const size_t pk = make_layout(D, W, E).total;
-  const size_t bt = sizeof(double) * E, bm = sizeof(int32_t) * E, bo = sizeof(int64_t) * (W + 1),
+  const size_t DD = (size_t)D * D;
+  // The batch is cut into kHostParts window ranges: part p's host->device copies (copy stream)
+  // overlap the fit of part p-1 (the caller's stream) and its results go back while part p+1
+  // fits, so the end-to-end time is one part's upload + the fits + one part's download.
+  // Windows are independent, so the results equal those of one call on the whole batch.
+  constexpr int kHostParts = 4;
+  const int P = W >= 4096 ? kHostParts : 1;
+  int64_t w0[kHostParts + 1];
+  for (int q = 0; q <= P; q++) w0[q] = W * q / P;
+  size_t pko[kHostParts + 1];
+  pko[0] = 0;
+  for (int q = 0; q < P; q++)
+    pko[q + 1] = pko[q] + align256(make_layout(D, w0[q + 1] - w0[q], off_h[w0[q + 1]] - off_h[w0[q]]).total);
+  const size_t bt = sizeof(double) * E, bm = sizeof(int32_t) * E, bo = sizeof(int64_t) * (W + P),
                bT = sizeof(double) * W, bth = sizeof(float) * W * D,
-               ba = sizeof(float) * W * D * D, bl = sizeof(double) * W, bi = sizeof(int32_t) * W;
+               ba = sizeof(float) * W * DD, bl = sizeof(double) * W, bi = sizeof(int32_t) * W;
   size_t off[12];
   size_t tot = 0;
-  const size_t sizes[11] = {bt, bm, bo, bT, bth, ba, ba, bl, bi, bi, pk};
+  const size_t sizes[11] = {bt, bm, bo, bT, bth, ba, ba, bl, bi, bi, pko[P]};
   for (int k = 0; k < 11; k++) {
     off[k] = tot;
     tot += align256(sizes[k]);
   }
   char* buf = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&buf), tot, st) != cudaSuccess) {
+  if (cudaMallocAsync(reinterpret_cast<void**>(&buf), tot, cs) != cudaSuccess) {
     set_error("cudaMallocAsync(%zu) failed", tot);
     return MDHP_ECUDA;
   }
   double* t_d = reinterpret_cast<double*>(buf + off[0]);
   int32_t* m_d = reinterpret_cast<int32_t*>(buf + off[1]);
-  int64_t* o_d = reinterpret_cast<int64_t*>(buf + off[2]);
+  int64_t* o_d = reinterpret_cast<int64_t*>(buf + off[2]);   // part q's offsets at o_d + w0[q] + q
   double* T_d = reinterpret_cast<double*>(buf + off[3]);
   float* th_d = reinterpret_cast<float*>(buf + off[4]);
   float* al_d = reinterpret_cast<float*>(buf + off[5]);
@@ -554,35 +571,79 @@ int mdhp_fit_host(const mdhp_pack_desc* d, const double* t_h, const int32_t* mar
   double* l_d = reinterpret_cast<double*>(buf + off[7]);
   int32_t* it_d = reinterpret_cast<int32_t*>(buf + off[8]);
   int32_t* s_d = reinterpret_cast<int32_t*>(buf + off[9]);
-  void* pk_d = buf + off[10];
-  auto h2d = [&](void* dst, const void* src, size_t n) {
-    return n == 0 || cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st) == cudaSuccess;
+  char* pk_d = buf + off[10];
+  cudaStream_t xs = nullptr;
+  cudaEvent_t ev_in[kHostParts] = {}, ev_fit[kHostParts] = {}, ev_buf = nullptr, ev_done = nullptr;
+  bool ok = cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ev_buf, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) == cudaSuccess;
+  for (int q = 0; q < P && ok; q++)
+    ok = cudaEventCreateWithFlags(&ev_in[q], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&ev_fit[q], cudaEventDisableTiming) == cudaSuccess;
+  auto cp = [&](void* dst, const void* src, size_t n, cudaMemcpyKind k) {
+    return n == 0 || cudaMemcpyAsync(dst, src, n, k, xs) == cudaSuccess;
   };
-  auto d2h = [&](void* dst, const void* src, size_t n) {
-    return n == 0 || cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st) == cudaSuccess;
-  };
-  bool ok = h2d(t_d, t_h, bt) && h2d(m_d, mark_h, bm) && h2d(o_d, off_h, bo) && h2d(T_d, T_h, bT) &&
-            h2d(th_d, theta_h, bth) && h2d(al_d, alpha_h, ba) && h2d(be_d, beta_h, ba);
-  if (!ok) {
-    cudaFreeAsync(buf, st);
-    set_error("host->device copy failed");
-    return MDHP_ECUDA;
+  // uploads: all parts in order on the copy stream (after the workspace exists)
+  ok = ok && cudaEventRecord(ev_buf, cs) == cudaSuccess && cudaStreamWaitEvent(xs, ev_buf, 0) == cudaSuccess;
+  for (int q = 0; q < P && ok; q++) {
+    const int64_t a = w0[q], z = w0[q + 1], e0 = off_h[a], e1 = off_h[z];
+    const cudaMemcpyKind H = cudaMemcpyHostToDevice;
+    ok = cp(t_d + e0, t_h + e0, sizeof(double) * (e1 - e0), H) &&
+         cp(m_d + e0, mark_h + e0, sizeof(int32_t) * (e1 - e0), H) &&
+         cp(o_d + a + q, off_h + a, sizeof(int64_t) * (z - a + 1), H) &&
+         cp(T_d + a, T_h + a, sizeof(double) * (z - a), H) &&
+         cp(th_d + a * D, theta_h + a * D, sizeof(float) * (z - a) * D, H) &&
+         cp(al_d + a * DD, alpha_h + a * DD, sizeof(float) * (z - a) * DD, H) &&
+         cp(be_d + a * DD, beta_h + a * DD, sizeof(float) * (z - a) * DD, H) &&
+         cudaEventRecord(ev_in[q], xs) == cudaSuccess;
   }
-  rc = mdhp_pack_windows(d, t_d, m_d, o_d, T_d, pk_d, pk, s_d, stream);
-  if (!rc) rc = mdhp_fit(d, pk_d, cfg, th_d, al_d, be_d, nullptr, l_d, it_d, s_d, nullptr, stream);
-  if (!rc) {
-    ok = d2h(theta_h, th_d, bth) && d2h(alpha_h, al_d, ba) && d2h(beta_h, be_d, ba) &&
-         d2h(lnl_h, l_d, bl) && d2h(iters_h, it_d, bi) && d2h(status_h, s_d, bi);
-    if (!ok) {
-      set_error("device->host copy failed");
+  if (!ok) set_error("host->device copies could not be enqueued");
+  // per part: rebase its offsets, pack, fit (caller's stream), then its results go back
+  for (int q = 0; q < P && ok && !rc; q++) {
+    const int64_t a = w0[q], z = w0[q + 1], e0 = off_h[a], e1 = off_h[z];
+    mdhp_pack_desc dq = *d;
+    dq.n_windows = z - a;
+    dq.n_events = e1 - e0;
+    ok = cudaStreamWaitEvent(cs, ev_in[q], 0) == cudaSuccess;
+    if (!ok) break;
+    int64_t* oq = o_d + a + q;
+    if (e0 != 0) rebase_offsets_launch(oq, z - a + 1, e0, cs);
+    void* pq = pk_d + pko[q];
+    rc = mdhp_pack_windows(&dq, t_d + e0, m_d + e0, oq, T_d + a, pq, pko[q + 1] - pko[q], s_d + a, cs);
+    if (!rc)
+      rc = mdhp_fit(&dq, pq, cfg, th_d + a * D, al_d + a * DD, be_d + a * DD, nullptr, l_d + a,
+                    it_d + a, s_d + a, nullptr, cs);
+    if (rc) break;
+    const cudaMemcpyKind B = cudaMemcpyDeviceToHost;
+    ok = cudaEventRecord(ev_fit[q], cs) == cudaSuccess && cudaStreamWaitEvent(xs, ev_fit[q], 0) == cudaSuccess &&
+         cp(theta_h + a * D, th_d + a * D, sizeof(float) * (z - a) * D, B) &&
+         cp(alpha_h + a * DD, al_d + a * DD, sizeof(float) * (z - a) * DD, B) &&
+         cp(beta_h + a * DD, be_d + a * DD, sizeof(float) * (z - a) * DD, B) &&
+         cp(lnl_h + a, l_d + a, sizeof(double) * (z - a), B) &&
+         cp(iters_h + a, it_d + a, sizeof(int32_t) * (z - a), B) &&
+         cp(status_h + a, s_d + a, sizeof(int32_t) * (z - a), B);
+    if (!ok) set_error("device->host copies could not be enqueued");
+  }
+  if (!ok && !rc) rc = MDHP_ECUDA;
+  // the workspace is freed on the caller's stream once the copy stream is done with it
+  if (xs) {
+    cudaEventRecord(ev_done, xs);
+    cudaStreamWaitEvent(cs, ev_done, 0);
+  }
+  cudaFreeAsync(buf, cs);
+  if ((xs && cudaStreamSynchronize(xs) != cudaSuccess) || cudaStreamSynchronize(cs) != cudaSuccess) {
+    if (!rc) {
+      set_error("stream sync failed: %s", cudaGetErrorString(cudaGetLastError()));
       rc = MDHP_ECUDA;
     }
   }
-  cudaFreeAsync(buf, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess && !rc) {
-    set_error("stream sync failed: %s", cudaGetErrorString(cudaGetLastError()));
-    rc = MDHP_ECUDA;
+  for (int q = 0; q < P; q++) {
+    if (ev_in[q]) cudaEventDestroy(ev_in[q]);
+    if (ev_fit[q]) cudaEventDestroy(ev_fit[q]);
   }
+  if (ev_buf) cudaEventDestroy(ev_buf);
+  if (ev_done) cudaEventDestroy(ev_done);
+  if (xs) cudaStreamDestroy(xs);
   return rc;
 }
 

@@ -290,4 +290,15 @@ int pack_launch(const mdhp_pack_desc* d, const double* t, const int32_t* mark,
   return MDHP_OK;
 }
 
+// mdhp_fit_host: a part's window offsets, copied as absolute event indices, made part-relative
+__global__ void k_rebase_offsets(int64_t* __restrict__ off, int64_t n, int64_t base) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) off[i] -= base;
+}
+
+void rebase_offsets_launch(int64_t* off, int64_t n, int64_t base, cudaStream_t st) {
+  k_rebase_offsets<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(off, n, base);
+  count_launch();
+}
+
 }  // namespace mdhp

@@ -395,3 +395,33 @@ def test_fit_masks_and_adam_hyperparameters(mask):
                 _param_close(g[k][w], o[w][k], what=f"mask{mask} w{w} {k}")
             else:
                 np.testing.assert_array_equal(g[k][w], f32(start[w]))
+
+
+def test_fit_host_pipelined_parts_equal_device_path():
+    """mdhp_fit_host with >= 4096 windows cuts the batch into parts whose uploads, fits and
+    downloads overlap on two streams; windows are independent, so every output equals one
+    pack + fit of the whole batch on device buffers, bit for bit (uneven part sizes, empty
+    windows included)."""
+    rng = np.random.default_rng(4242)
+    D, W = 3, 4099
+    wins = []
+    for w in range(W):
+        n = int(rng.integers(0, 40)) if w % 97 else 0
+        wins.append((np.sort(rng.uniform(0.0, 1.0, n)), rng.integers(0, D, n).astype(np.int32)))
+    b = H.batch_from_windows(wins, 1.0)
+    cfg = M.FitConfig(max_iters=8, tol_rel=0.0)
+    th = torch.full((W, D), 3.0); al = torch.full((W, D, D), 0.7); be = torch.full((W, D, D), 9.0)
+    th_d, al_d, be_d = th.to(DEV), al.to(DEV), be.to(DEV)
+    pin = lambda x: x.pin_memory()
+    thp, alp, bep = pin(th.clone()), pin(al.clone()), pin(be.clone())
+    r = M.fit_host(D, pin(torch.tensor(b["t"])), pin(torch.tensor(b["mark"])), pin(torch.tensor(b["win_off"])),
+                   pin(torch.tensor(b["T"])), thp, alp, bep, cfg)
+    pk = M.pack_windows(D, *dev_batch(b))
+    rd = M.fit(pk, th_d, al_d, be_d, cfg)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(thp.numpy(), th_d.cpu().numpy())
+    np.testing.assert_array_equal(alp.numpy(), al_d.cpu().numpy())
+    np.testing.assert_array_equal(bep.numpy(), be_d.cpu().numpy())
+    np.testing.assert_array_equal(r["lnl"].numpy(), rd["lnl"].cpu().numpy())
+    np.testing.assert_array_equal(r["iters"].numpy(), rd["iters"].cpu().numpy())
+    np.testing.assert_array_equal(r["status"].numpy(), rd["status"].cpu().numpy())
