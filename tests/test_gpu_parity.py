@@ -397,7 +397,8 @@ def test_fit_masks_and_adam_hyperparameters(mask):
                 np.testing.assert_array_equal(g[k][w], f32(start[w]))
 
 
-def test_fit_host_pipelined_parts_equal_device_path():
+@pytest.mark.parametrize("pinned", [True, False])
+def test_fit_host_pipelined_parts_equal_device_path(pinned):
     """mdhp_fit_host with >= 4096 windows cuts the batch into parts whose uploads, fits and
     downloads overlap on two streams; windows are independent, so every output equals one
     pack + fit of the whole batch on device buffers, bit for bit (uneven part sizes, empty
@@ -412,7 +413,7 @@ def test_fit_host_pipelined_parts_equal_device_path():
     cfg = M.FitConfig(max_iters=8, tol_rel=0.0)
     th = torch.full((W, D), 3.0); al = torch.full((W, D, D), 0.7); be = torch.full((W, D, D), 9.0)
     th_d, al_d, be_d = th.to(DEV), al.to(DEV), be.to(DEV)
-    pin = lambda x: x.pin_memory()
+    pin = (lambda x: x.pin_memory()) if pinned else (lambda x: x.contiguous())
     thp, alp, bep = pin(th.clone()), pin(al.clone()), pin(be.clone())
     r = M.fit_host(D, pin(torch.tensor(b["t"])), pin(torch.tensor(b["mark"])), pin(torch.tensor(b["win_off"])),
                    pin(torch.tensor(b["T"])), thp, alp, bep, cfg)
