@@ -202,10 +202,17 @@ __device__ __forceinline__ void store_params(const float2* A, const WarpCtx<DP>&
   }
 }
 
-// Persistent fit kernel: each warp takes G windows at a time (longest first) from a global
-// counter and runs their whole iteration loop on chip (a6), then evaluates lnL at the final
-// parameters and writes everything back.
-template <int DP, bool RESUME>
+// Persistent fit kernel (a6): windows are taken longest first from a global counter and run
+// their whole iteration loop on chip, then lnL is evaluated at the returned parameters and
+// everything is written back.
+//   REFILL (converged mode, tol_rel > 0): each group of DP lanes takes one window at a time;
+//     when its window stops (convergence, divergence, budget) the group evaluates the final lnL,
+//     writes back and takes the next window at once, so a warp's other group(s) never idle
+//     behind a window that stopped early (the convergence mask frees lanes instead of padding
+//     them).  One evaluation per warp step: TRAIN groups step after it, FINAL groups record it.
+//   !REFILL (fixed iteration count): every window of a warp stops at the same evaluation, so a
+//     warp takes G windows at a time and keeps them to the end (no per-window bookkeeping).
+template <int DP, bool RESUME, bool REFILL>
 __global__ void __launch_bounds__(128, DP >= 32 ? 2 : 4)
 k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ alpha,
       float* __restrict__ beta, float* __restrict__ opt, double* __restrict__ lnl_out,
@@ -220,33 +227,54 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
   float2* SQ = gbase_s + SM::AS;
   float2* Gs = gbase_s + 2 * SM::AS;
   const int D = P.D;
-  const int64_t nunits = (P.W + SM::G - 1) / SM::G;
-  for (;;) {
-    int64_t unit = 0;
-    if (c.lane == 0) unit = atomicAdd(counter, 1);
-    unit = __shfl_sync(kFull, unit, 0);
-    if (unit >= nunits) break;
-    const int64_t slot = unit * SM::G + c.g;
-    const int64_t w = slot < P.W ? P.perm[slot] : 0;
-    MDHP_ASSERT(w >= 0 && w < (P.W > 0 ? P.W : 1));
-    const int st0 = slot < P.W ? status[w] : MDHP_ST_INVALID;
-    const bool live = slot < P.W && !(st0 & MDHP_ST_INVALID);
-    float th = load_params<DP>(A, c, D, w, live, theta, alpha, beta);
-    const ColInfo ci = col_info<DP>(P, w, live, c.j);
-    const int n = live ? P.n[w] : 0;
-    const float scale = (cfg.loss_mean && n > 0) ? 1.0f / (float)n : 1.0f;
-    // per-window (group-uniform) optimizer state
-    int it = 0, s = 0, halv = 0, stall = 0, st = 0;
-    float lr_w = cfg.lr;
+  if constexpr (REFILL) {
+    enum { TRAIN = 0, FINAL = 1, IDLE = 2 };
+    // per-group (group-uniform) window and optimizer state
+    int phase = IDLE;
+    int64_t w = 0;
+    int st0 = 0, n = 0, it = 0, s = 0, halv = 0, stall = 0, st = 0;
+    bool live = false, have_prev = false, have_lnl = false;
+    float th = 0.0f, scale = 1.0f, lr_w = cfg.lr;
     double lnl_prev = 0.0;
-    bool have_prev = false, have_lnl = false;
-    bool done = !live || cfg.max_iters <= 0;
-    while (__any_sync(kFull, !done)) {
-      const int nmax = group_max_i<DP>(done ? 0 : n);
+    ColInfo ci = col_info<DP>(P, 0, false, c.j);
+    // group-collective: take the next window (all lanes of the group, none of the others)
+    auto fetch = [&]() {
+      int64_t slot = 0;
+      if (c.j == 0) slot = atomicAdd(counter, 1);
+      slot = __shfl_sync(c.gmask, slot, c.gbase);
+      if (slot >= P.W) {
+        phase = IDLE;
+        live = false;
+        n = 0;
+        return;
+      }
+      w = P.perm[slot];
+      MDHP_ASSERT(w >= 0 && w < P.W);
+      st0 = status[w];
+      live = !(st0 & MDHP_ST_INVALID);
+      th = load_params<DP>(A, c, D, w, live, theta, alpha, beta);
+      ci = col_info<DP>(P, w, live, c.j);
+      n = live ? P.n[w] : 0;
+      scale = (cfg.loss_mean && n > 0) ? 1.0f / (float)n : 1.0f;
+      it = s = halv = stall = st = 0;
+      lr_w = cfg.lr;
+      lnl_prev = 0.0;
+      have_prev = have_lnl = false;
+      phase = (!live || cfg.max_iters <= 0) ? FINAL : TRAIN;
+    };
+    fetch();
+    while (__any_sync(kFull, phase != IDLE)) {
+      const bool act = phase != IDLE && live;
+      const int nmax = group_max_i<DP>(act ? n : 0);
       float dth;
       bool finite;
-      const double lnl = eval_window<DP, true>(P, A, SQ, Gs, c, w, !done, nmax, th, ci, dth, finite);
-      if (!done) {
+      // gradients only when some group trains (a warp whose groups all stop together, as in the
+      // fixed-iteration mode, evaluates its final lnL without them)
+      const double lnl = __any_sync(kFull, phase == TRAIN)
+                             ? eval_window<DP, true>(P, A, SQ, Gs, c, w, act, nmax, th, ci, dth, finite)
+                             : eval_window<DP, false>(P, A, SQ, Gs, c, w, act, nmax, th, ci, dth, finite);
+      if (phase == TRAIN) {
+        bool done = false;
         if (!finite) {
           st |= MDHP_ST_NONFINITE;
           if (!have_prev || halv >= cfg.max_halvings) {
@@ -280,25 +308,103 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
           }
         }
         if (it >= cfg.max_iters) done = true;
+        if (done) phase = FINAL;   // the next evaluation is lnL at the returned parameters
+      } else if (phase == FINAL) {
+        if (live) store_params<DP>(A, c, D, w, th, theta, alpha, beta);
+        if (c.j == 0) {
+          lnl_out[w] = live ? lnl : (double)NAN;
+          iters_out[w] = it;
+          status[w] = st0 | st;
+          if (trace && live)
+            for (int q = it; q < cfg.max_iters; q++) trace[(size_t)w * cfg.max_iters + q] = NAN;
+        }
+        fetch();
       }
       __syncwarp();
     }
-    // lnL at the returned parameters (no gradient accumulation needed)
-    const int nmax = group_max_i<DP>(n);
-    float dth;
-    bool finite;
-    const double lnl = eval_window<DP, false>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite);
-    if (slot < P.W) {
-      if (live) store_params<DP>(A, c, D, w, th, theta, alpha, beta);
-      if (c.j == 0) {
-        lnl_out[w] = live ? lnl : (double)NAN;
-        iters_out[w] = it;
-        status[w] = st0 | st;
-        if (trace && live)
-          for (int q = it; q < cfg.max_iters; q++) trace[(size_t)w * cfg.max_iters + q] = NAN;
+  } else {
+    // fixed iteration count: every window of a warp stops at the same evaluation, so the
+    // warp keeps its G windows to the end (no per-window refill bookkeeping)
+    const int64_t nunits = (P.W + SM::G - 1) / SM::G;
+    for (;;) {
+      int64_t unit = 0;
+      if (c.lane == 0) unit = atomicAdd(counter, 1);
+      unit = __shfl_sync(kFull, unit, 0);
+      if (unit >= nunits) break;
+      const int64_t slot = unit * SM::G + c.g;
+      const int64_t w = slot < P.W ? P.perm[slot] : 0;
+      MDHP_ASSERT(w >= 0 && w < (P.W > 0 ? P.W : 1));
+      const int st0 = slot < P.W ? status[w] : MDHP_ST_INVALID;
+      const bool live = slot < P.W && !(st0 & MDHP_ST_INVALID);
+      float th = load_params<DP>(A, c, D, w, live, theta, alpha, beta);
+      const ColInfo ci = col_info<DP>(P, w, live, c.j);
+      const int n = live ? P.n[w] : 0;
+      const float scale = (cfg.loss_mean && n > 0) ? 1.0f / (float)n : 1.0f;
+      // per-window (group-uniform) optimizer state
+      int it = 0, s = 0, halv = 0, stall = 0, st = 0;
+      float lr_w = cfg.lr;
+      double lnl_prev = 0.0;
+      bool have_prev = false, have_lnl = false;
+      bool done = !live || cfg.max_iters <= 0;
+      while (__any_sync(kFull, !done)) {
+        const int nmax = group_max_i<DP>(done ? 0 : n);
+        float dth;
+        bool finite;
+        const double lnl = eval_window<DP, true>(P, A, SQ, Gs, c, w, !done, nmax, th, ci, dth, finite);
+        if (!done) {
+          if (!finite) {
+            st |= MDHP_ST_NONFINITE;
+            if (!have_prev || halv >= cfg.max_halvings) {
+              st |= MDHP_ST_DIVERGED;
+              done = true;
+              if (have_prev) th = load_params<DP>(A, c, D, w, true, theta, alpha, beta);
+            } else {
+              th = load_params<DP>(A, c, D, w, true, theta, alpha, beta);
+              lr_w *= 0.5f;
+              halv++;
+              it++;
+            }
+          } else {
+            if (trace && c.j == 0) trace[(size_t)w * cfg.max_iters + it] = (float)lnl;
+            if (cfg.tol_rel > 0.0f && have_lnl) {
+              const double thr = (double)cfg.tol_rel * fmax(fabs(lnl_prev), 1.0);
+              stall = (fabs(lnl - lnl_prev) <= thr) ? stall + 1 : 0;
+              if (stall >= cfg.patience) {
+                st |= MDHP_ST_CONVERGED;
+                done = true;
+              }
+            }
+            if (!done) {
+              lnl_prev = lnl;
+              have_lnl = true;
+              store_params<DP>(A, c, D, w, th, theta, alpha, beta);   // previous point
+              have_prev = true;
+              s++;
+              step_column<DP, RESUME>(A, Gs, c, D, w, cfg, lr_w, s, scale, dth, th, opt);
+              it++;
+            }
+          }
+          if (it >= cfg.max_iters) done = true;
+        }
+        __syncwarp();
       }
+      // lnL at the returned parameters (no gradient accumulation needed)
+      const int nmax = group_max_i<DP>(n);
+      float dth;
+      bool finite;
+      const double lnl = eval_window<DP, false>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite);
+      if (slot < P.W) {
+        if (live) store_params<DP>(A, c, D, w, th, theta, alpha, beta);
+        if (c.j == 0) {
+          lnl_out[w] = live ? lnl : (double)NAN;
+          iters_out[w] = it;
+          status[w] = st0 | st;
+          if (trace && live)
+            for (int q = it; q < cfg.max_iters; q++) trace[(size_t)w * cfg.max_iters + q] = NAN;
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
@@ -345,7 +451,9 @@ static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float*
   using SM = Smem<DP>;
   constexpr int WPB = 4;
   const size_t smem = WPB * SM::per_warp;
-  auto kern = cfg.step0 != 0 ? k_fit<DP, true> : k_fit<DP, false>;
+  // converged mode (tol_rel > 0): windows stop at different iterations -> per-window refill
+  auto kern = cfg.tol_rel > 0.0f ? (cfg.step0 != 0 ? k_fit<DP, true, true> : k_fit<DP, false, true>)
+                                 : (cfg.step0 != 0 ? k_fit<DP, true, false> : k_fit<DP, false, false>);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess) {
     set_error("cudaFuncSetAttribute(k_fit) failed");

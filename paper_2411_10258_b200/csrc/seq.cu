@@ -323,7 +323,6 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
   constexpr int G = 32 / DP, RS = DP + 1;
   extern __shared__ __align__(16) unsigned char smem_l[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / DP, j = lane % DP;
-  const int gbase = g * DP;
   float2* SQ = reinterpret_cast<float2*>(smem_l) + (size_t)(wid * G + g) * DP * RS;
   float* B = reinterpret_cast<float*>(reinterpret_cast<float2*>(smem_l) + (size_t)4 * G * DP * RS) +
              (size_t)(wid * G + g) * DP * RS;

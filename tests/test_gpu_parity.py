@@ -426,3 +426,35 @@ def test_fit_host_pipelined_parts_equal_device_path(pinned):
     np.testing.assert_array_equal(r["lnl"].numpy(), rd["lnl"].cpu().numpy())
     np.testing.assert_array_equal(r["iters"].numpy(), rd["iters"].cpu().numpy())
     np.testing.assert_array_equal(r["status"].numpy(), rd["status"].cpu().numpy())
+
+
+def test_converged_mode_refill_is_batch_invariant():
+    """Converged mode (tol_rel > 0) lets a group take its next window as soon as its window
+    stops; no state may leak from one window to the next: every window's parameters, lnL,
+    iteration count and status are bit-identical to fitting it alone, and windows do
+    stop at different iterations here."""
+    rng = np.random.default_rng(777)
+    D, W = 5, 300
+    wins = []
+    for w in range(W):
+        n = int(rng.integers(5, 200))
+        wins.append((np.sort(rng.uniform(0.0, 1.0, n)), rng.integers(0, D, n).astype(np.int32)))
+    b = H.batch_from_windows(wins, 1.0)
+    th0 = rng.uniform(2.0, 40.0, (W, D)); al0 = rng.uniform(0.1, 5.0, (W, D, D)); be0 = rng.uniform(5.0, 60.0, (W, D, D))
+    cfg = M.FitConfig(max_iters=300, optimizer="adam", lr=0.05, tol_rel=1e-4, patience=5)
+
+    def run(bb, th, al, be):
+        pk = M.pack_windows(D, *dev_batch(bb))
+        tt = [torch.tensor(f32(x), device=DEV) for x in (th, al, be)]
+        r = M.fit(pk, *tt, cfg)
+        torch.cuda.synchronize()
+        return [x.cpu().numpy() for x in tt] + [r["lnl"].cpu().numpy(), r["iters"].cpu().numpy(),
+                                                r["status"].cpu().numpy()]
+    full = run(b, th0, al0, be0)
+    assert len(np.unique(full[4])) > 5          # windows stopped at many different iterations
+    for w in (0, 1, 17, 150, 298, 299):
+        a, z = b["win_off"][w], b["win_off"][w + 1]
+        one = run(H.batch_from_windows([(b["t"][a:z], b["mark"][a:z])], 1.0), th0[w:w + 1], al0[w:w + 1],
+                  be0[w:w + 1])
+        for k in range(6):
+            np.testing.assert_array_equal(one[k][0], full[k][w], err_msg=f"window {w} output {k}")
