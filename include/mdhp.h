@@ -136,12 +136,28 @@ int mdhp_pack_windows(const mdhp_pack_desc* desc, const double* t, const int32_t
  *   d beta_ij  = -alpha_ij sum_{n in i} Q_ij(t_n)/lambda_n + alpha_ij H_ij / beta_ij^2, with
  *   R, Q the decayed sums of Eq.(2) and of (t - t_k) times its terms, E_ij = sum_k (e^{-b u_k} - 1),
  *   H_ij = sum_k (1 - e^{-b u_k}(1 + b u_k)).
- * Asynchronous.
+ * Precision: fp32 evaluation; windows whose fp32 lnL could miss 1e-4 relative (R24)
+ * are re-evaluated in fp64 on the GPU (lnL and gradients; see mdhp_loglik_exact).
+ * Asynchronous (one stream-ordered workspace of 256 + 4 W bytes).
  */
 int mdhp_loglik_grad(const mdhp_pack_desc* desc, const void* packed,
                      const float* theta, const float* alpha, const float* beta,
                      double* loglik, float* g_theta, float* g_alpha, float* g_beta,
                      const int32_t* win_status, void* stream);
+
+/*
+ * mdhp_loglik_exact — the same outputs as mdhp_loglik_grad, every window evaluated in fp64 on
+ * the GPU (state, exponentials, logarithms and sums in double, from the packed fp32 analysis
+ * times; Part3 terms summed directly as sum_k expm1(-beta u_k)).  mdhp_loglik_grad and
+ * mdhp_fit run this evaluation automatically on the windows whose fp32 lnL could miss 1e-4
+ * relative (R24: lnL a cancellation of much larger terms); this entry point applies
+ * it to the whole batch (reference-quality GPU evaluation, ~100x the fp32 cost).
+ * Same arguments and layout as mdhp_loglik_grad.  Asynchronous.
+ */
+int mdhp_loglik_exact(const mdhp_pack_desc* desc, const void* packed,
+                      const float* theta, const float* alpha, const float* beta,
+                      double* loglik, float* g_theta, float* g_alpha, float* g_beta,
+                      const int32_t* win_status, void* stream);
 
 /*
  * mdhp_loglik_dense — ABLATION: lnL of Eq.(5) evaluated the way the
@@ -188,9 +204,12 @@ typedef struct {
  *   opt_state [W][2][D + 2 D^2] fp32 Adam moments (m then v, each in theta|alpha|beta order),
  *             in/out; NULL -> zero-initialised internal workspace (resume = pass it back
  *             with cfg->adam_step0 = the iterations already run)
- *   loglik [W]   fp64 out: lnL at the returned parameters
+ *   loglik [W]   fp64 out: lnL at the returned parameters (fp32 evaluation, fp64 on the GPU for
+ *                the windows of DESIGN.md R24)
  *   iters  [W]   int32 out: iterations run
- *   win_status [W] in: from mdhp_pack_windows; out: OR-ed with NONFINITE / DIVERGED / CONVERGED
+ *   win_status [W] in: from mdhp_pack_windows; out: its validation bits (MDHP_ST_INVALID | EMPTY)
+ *                OR-ed with this call's NONFINITE / DIVERGED / CONVERGED (outcome bits of an
+ *                earlier call on the same batch are not carried over)
  *   lnl_trace [W][max_iters] fp32 out or NULL: lnL of every evaluation (NaN after the stop)
  * One persistent kernel launch for the iteration loop (+1 for workspace init).  Asynchronous.
  */

@@ -9,7 +9,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libmdhp.so")
 LIB_DEBUG = os.path.join(LIBDIR, "libmdhp_debug.so")   # -DMDHP_DEBUG: device bounds asserts
-SOURCES = ["abi.cu", "pack.cu", "fit.cu", "seq.cu", "dense.cu", "features.cu"]
+SOURCES = ["abi.cu", "pack.cu", "fit.cu", "exact.cu", "seq.cu", "dense.cu", "features.cu"]
 HEADERS = ["common.cuh", "eval.cuh"]
 CC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
             "-Xcompiler", "-fPIC"]

@@ -13,10 +13,14 @@ int pack_launch(const mdhp_pack_desc* d, const double* t, const int32_t* mark,
                 const int64_t* win_off, const double* T, void* packed, int32_t* win_status,
                 cudaStream_t st);
 int loglik_launch(const Packed& P, const float* th, const float* al, const float* be, double* lnl,
-                  float* gt, float* ga, float* gb, const int32_t* status, cudaStream_t st);
+                  float* gt, float* ga, float* gb, const int32_t* status, int32_t* xlist,
+                  int32_t* xcount, cudaStream_t st);
 int fit_launch(const Packed& P, const FitCfgDev& cfg, float* th, float* al, float* be, float* opt,
                double* lnl, int32_t* iters, int32_t* status, float* trace, int* counter,
-               cudaStream_t st);
+               int32_t* xlist, int32_t* xcount, cudaStream_t st);
+int exact_launch(const Packed& P, const float* th, const float* al, const float* be,
+                 const int32_t* list, const int32_t* count, double* lnl, float* gt, float* ga,
+                 float* gb, const int32_t* status, cudaStream_t st);
 
 int features_launch(int D, int64_t W, int H, const float* theta, const float* alpha,
                     const float* beta, const float* T, const float* A, const float* B,
@@ -151,6 +155,21 @@ static int check_cfg(const mdhp_fit_config* c) {
   return MDHP_OK;
 }
 
+// Raise the release threshold of the current device's default memory pool (once per device)
+// so that the stream-ordered workspaces of repeated calls are reused instead of being unmapped
+// and re-mapped at every synchronisation (tens of GB for mdhp_fit_host at cfg5 scale).
+static void keep_pool_memory() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 }  // namespace mdhp
 
 using namespace mdhp;
@@ -217,10 +236,52 @@ int mdhp_loglik_grad(const mdhp_pack_desc* d, const void* packed, const float* t
   }
   const Layout L = make_layout(d->D, d->n_windows, d->n_events);
   const Packed P = view(L, packed);
-  rc = loglik_launch(P, theta, alpha, beta, loglik, g_theta, g_alpha, g_beta, win_status,
-                     (cudaStream_t)stream);
+  if (P.W == 0) return MDHP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  // workspace: the count and list of windows re-evaluated in fp64 (exact.cu)
+  keep_pool_memory();
+  void* ws = nullptr;
+  const size_t ws_bytes = 256 + sizeof(int32_t) * (size_t)P.W;
+  if (cudaMallocAsync(&ws, ws_bytes, st) != cudaSuccess) {
+    set_error("cudaMallocAsync(%zu) failed", ws_bytes);
+    return MDHP_ECUDA;
+  }
+  int32_t* xcount = static_cast<int32_t*>(ws);
+  int32_t* xlist = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + 256);
+  if (cudaMemsetAsync(xcount, 0, sizeof(int32_t), st) != cudaSuccess) {
+    cudaFreeAsync(ws, st);
+    set_error("cudaMemsetAsync failed");
+    return MDHP_ECUDA;
+  }
+  rc = loglik_launch(P, theta, alpha, beta, loglik, g_theta, g_alpha, g_beta, win_status, xlist,
+                     xcount, st);
+  if (!rc)
+    rc = exact_launch(P, theta, alpha, beta, xlist, xcount, loglik, g_theta, g_alpha, g_beta,
+                      win_status, st);
+  cudaFreeAsync(ws, st);
   if (rc) return rc;
   return check_cuda("mdhp_loglik_grad");
+}
+
+int mdhp_loglik_exact(const mdhp_pack_desc* d, const void* packed, const float* theta,
+                      const float* alpha, const float* beta, double* loglik, float* g_theta,
+                      float* g_alpha, float* g_beta, const int32_t* win_status, void* stream) {
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!packed || !theta || !alpha || !beta || !loglik || !win_status) {
+    set_error("NULL pointer argument");
+    return MDHP_EINVAL;
+  }
+  const bool any = g_theta || g_alpha || g_beta, all = g_theta && g_alpha && g_beta;
+  if (any && !all) {
+    set_error("g_theta, g_alpha, g_beta must be all NULL or all non-NULL");
+    return MDHP_EINVAL;
+  }
+  const Layout L = make_layout(d->D, d->n_windows, d->n_events);
+  rc = exact_launch(view(L, packed), theta, alpha, beta, nullptr, nullptr, loglik, g_theta,
+                    g_alpha, g_beta, win_status, (cudaStream_t)stream);
+  if (rc) return rc;
+  return check_cuda("mdhp_loglik_exact");
 }
 
 int mdhp_loglik_dense(const mdhp_pack_desc* d, const void* packed, const float* theta,
@@ -236,21 +297,6 @@ int mdhp_loglik_dense(const mdhp_pack_desc* d, const void* packed, const float* 
   rc = dense_launch(view(L, packed), theta, alpha, beta, loglik, win_status, (cudaStream_t)stream);
   if (rc) return rc;
   return check_cuda("mdhp_loglik_dense");
-}
-
-// Raise the release threshold of the current device's default memory pool (once per device)
-// so that the stream-ordered workspaces of repeated calls are reused instead of being unmapped
-// and re-mapped at every synchronisation (tens of GB for mdhp_fit_host at cfg5 scale).
-static void keep_pool_memory() {
-  static bool done[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done[dev] = true;
 }
 
 int mdhp_hawkes_features(int32_t D, int64_t W, int32_t H, const float* theta,
@@ -297,10 +343,12 @@ int mdhp_fit(const mdhp_pack_desc* d, const void* packed, const mdhp_fit_config*
   const int64_t W = d->n_windows;
   if (W == 0) return MDHP_OK;
   const size_t PP = (size_t)d->D + 2 * (size_t)d->D * d->D;
-  // workspace: work counter (+ zero-initialised Adam moments when the caller passes none)
+  // workspace: work counter and the fp64 re-evaluation count (256 B), the re-evaluation list,
+  // (+ zero-initialised Adam moments when the caller passes none)
   keep_pool_memory();
   const bool own_opt = opt_state == nullptr && cfg->optimizer == MDHP_OPT_ADAM;
-  size_t ws_bytes = 256 + (own_opt ? sizeof(float) * 2 * PP * (size_t)W : 0);
+  const size_t list_bytes = align256(sizeof(int32_t) * (size_t)W);
+  size_t ws_bytes = 256 + list_bytes + (own_opt ? sizeof(float) * 2 * PP * (size_t)W : 0);
   void* ws = nullptr;
   if (cudaMallocAsync(&ws, ws_bytes, st) != cudaSuccess) {
     set_error("cudaMallocAsync(%zu) failed", ws_bytes);
@@ -312,7 +360,9 @@ int mdhp_fit(const mdhp_pack_desc* d, const void* packed, const mdhp_fit_config*
     return MDHP_ECUDA;
   }
   int* counter = static_cast<int*>(ws);
-  float* opt = own_opt ? reinterpret_cast<float*>(static_cast<char*>(ws) + 256) : opt_state;
+  int32_t* xcount = static_cast<int32_t*>(ws) + 1;
+  int32_t* xlist = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + 256);
+  float* opt = own_opt ? reinterpret_cast<float*>(static_cast<char*>(ws) + 256 + list_bytes) : opt_state;
   FitCfgDev c;
   c.max_iters = cfg->max_iters;
   c.optimizer = cfg->optimizer;
@@ -327,7 +377,12 @@ int mdhp_fit(const mdhp_pack_desc* d, const void* packed, const mdhp_fit_config*
   c.tol_rel = cfg->tol_rel;
   c.min_param = cfg->min_param;
   c.fit_mask = cfg->fit_mask;
-  rc = fit_launch(P, c, theta, alpha, beta, opt, loglik, iters, win_status, lnl_trace, counter, st);
+  rc = fit_launch(P, c, theta, alpha, beta, opt, loglik, iters, win_status, lnl_trace, counter,
+                  xlist, xcount, st);
+  // lnL at the returned parameters again in fp64 where the fp32 value may miss 1e-4 relative
+  if (!rc)
+    rc = exact_launch(P, theta, alpha, beta, xlist, xcount, loglik, nullptr, nullptr, nullptr,
+                      win_status, st);
   cudaFreeAsync(ws, st);
   if (rc) return rc;
   return check_cuda("mdhp_fit");

@@ -25,6 +25,15 @@ constexpr int kSortBuckets = 65536;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr unsigned kFull = 0xffffffffu;
+// fp64 re-evaluation threshold (fit.cu needs_exact, R24): a window is re-evaluated in
+// fp64 unless |lnL| >= kExactPerEvent N + kExactPerLn |sum ln lambda| + kExactGross (|Part2| +
+// |Part3|)
+constexpr double kExactPerEvent = 0.05;
+constexpr double kExactPerLn = 0.01;
+constexpr double kExactGross = 0.02;
+// status bits a fit call keeps from its input (validation); the fit's own outcome bits
+// (NONFINITE, DIVERGED, CONVERGED) are those of this call only
+constexpr int kKeepStatus = MDHP_ST_INVALID | MDHP_ST_EMPTY;
 
 inline int pad_dims(int D) {
   int p = 1;

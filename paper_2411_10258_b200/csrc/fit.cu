@@ -18,14 +18,33 @@ struct WarpCtx {
   }
 };
 
+// Whether the fp32 lnL of a window may be off by more than 1e-4 |lnL| (R24): the
+// absolute error of the fp32 evaluation is bounded by a few ulps per event of ln lambda
+// (lambda itself carries O(10) ulps after the recurrence; lg2.approx adds ~2 ulps of |lg2|)
+// plus a few ulps of the compensator |Part2| + |Part3|.  A window is re-evaluated in fp64
+// (exact.cu) when those bounds, with a safety factor of ~6 over the worst error measured in
+// the fuzz sweep (13 ulps per event), are not below 1e-4 |lnL|.
+__device__ __forceinline__ bool needs_exact(double lnl, int n, double sum_ln, double part2,
+                                            double part3) {
+  return !(fabs(lnl) >= kExactPerEvent * (double)n + kExactPerLn * fabs(sum_ln) +
+                            kExactGross * (fabs(part2) + fabs(part3)));
+}
+
+// Append window w to the fp64 re-evaluation list (one lane per group).
+__device__ __forceinline__ void list_exact(int32_t* list, int32_t* count, int64_t w) {
+  const int q = atomicAdd(count, 1);
+  list[q] = (int32_t)w;
+}
+
 // Evaluate the window owned by this group at the parameters in K (alpha, beta) / th.
 // Writes gradients (d alpha, d beta) over the accumulators in Gs when GRAD; returns lnL
-// (identical in every lane of the group) and this lane's d theta_j.
+// (identical in every lane of the group) and this lane's d theta_j; `exact` tells whether the
+// window needs the fp64 re-evaluation (needs_exact).
 template <int DP, bool GRAD>
 __device__ __forceinline__ double eval_window(const Packed& P, float2* A, float2* SQ, float2* Gs,
                                               const WarpCtx<DP>& c, int64_t w, bool live,
                                               int nmax, float th, const ColInfo& ci,
-                                              float& dth, bool& finite) {
+                                              float& dth, bool& finite, bool& exact) {
   reset_state<DP>(SQ, Gs, c.j);
   __syncwarp();
   const int n = live ? P.n[w] : 0;
@@ -66,6 +85,7 @@ __device__ __forceinline__ double eval_window(const Packed& P, float2* A, float2
   const double lnl = (double)kLn2 * lsum + part3 - (double)ci.T * sth;
   const unsigned bal = __ballot_sync(kFull, ok) & c.gmask;
   finite = (bal == c.gmask) && isfinite(lnl);
+  exact = live && needs_exact(lnl, n, (double)kLn2 * lsum, (double)ci.T * sth, part3);
   return lnl;
 }
 
@@ -107,7 +127,8 @@ __global__ void __launch_bounds__(128, DP >= 32 ? 2 : 4)
 k_loglik(Packed P, const float* __restrict__ theta, const float* __restrict__ alpha,
          const float* __restrict__ beta, double* __restrict__ lnl_out,
          float* __restrict__ g_theta, float* __restrict__ g_alpha, float* __restrict__ g_beta,
-         const int32_t* __restrict__ status) {
+         const int32_t* __restrict__ status, int32_t* __restrict__ xlist,
+         int32_t* __restrict__ xcount) {
   extern __shared__ __align__(16) unsigned char smem[];
   using SM = Smem<DP>;
   WarpCtx<DP> c;
@@ -125,13 +146,16 @@ k_loglik(Packed P, const float* __restrict__ theta, const float* __restrict__ al
   const ColInfo ci = col_info<DP>(P, w, live, c.j);
   const int nmax = group_max_i<DP>(live ? P.n[w] : 0);
   float dth;
-  bool finite;
+  bool finite, exact;
   const bool grad = g_theta != nullptr;
   double lnl;
-  if (grad) lnl = eval_window<DP, true>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite);
-  else lnl = eval_window<DP, false>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite);
+  if (grad) lnl = eval_window<DP, true>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite, exact);
+  else lnl = eval_window<DP, false>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite, exact);
   if (slot >= P.W) return;
-  if (c.j == 0) lnl_out[w] = live ? lnl : (double)NAN;
+  if (c.j == 0) {
+    lnl_out[w] = live ? lnl : (double)NAN;
+    if (exact) list_exact(xlist, xcount, w);
+  }
   if (grad && c.j < D) {
     g_theta[(size_t)w * D + c.j] = live ? dth : NAN;
     for (int i = 0; i < D; i++) {
@@ -217,7 +241,8 @@ __global__ void __launch_bounds__(128, DP >= 32 ? 2 : 4)
 k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ alpha,
       float* __restrict__ beta, float* __restrict__ opt, double* __restrict__ lnl_out,
       int32_t* __restrict__ iters_out, int32_t* __restrict__ status,
-      float* __restrict__ trace, int* __restrict__ counter) {
+      float* __restrict__ trace, int* __restrict__ counter, int32_t* __restrict__ xlist,
+      int32_t* __restrict__ xcount) {
   extern __shared__ __align__(16) unsigned char smem[];
   using SM = Smem<DP>;
   WarpCtx<DP> c;
@@ -267,12 +292,12 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
       const bool act = phase != IDLE && live;
       const int nmax = group_max_i<DP>(act ? n : 0);
       float dth;
-      bool finite;
+      bool finite, exact;
       // gradients only when some group trains (a warp whose groups all stop together, as in the
       // fixed-iteration mode, evaluates its final lnL without them)
       const double lnl = __any_sync(kFull, phase == TRAIN)
-                             ? eval_window<DP, true>(P, A, SQ, Gs, c, w, act, nmax, th, ci, dth, finite)
-                             : eval_window<DP, false>(P, A, SQ, Gs, c, w, act, nmax, th, ci, dth, finite);
+                             ? eval_window<DP, true>(P, A, SQ, Gs, c, w, act, nmax, th, ci, dth, finite, exact)
+                             : eval_window<DP, false>(P, A, SQ, Gs, c, w, act, nmax, th, ci, dth, finite, exact);
       if (phase == TRAIN) {
         bool done = false;
         if (!finite) {
@@ -314,7 +339,8 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
         if (c.j == 0) {
           lnl_out[w] = live ? lnl : (double)NAN;
           iters_out[w] = it;
-          status[w] = st0 | st;
+          status[w] = (st0 & kKeepStatus) | st;
+          if (exact) list_exact(xlist, xcount, w);
           if (trace && live)
             for (int q = it; q < cfg.max_iters; q++) trace[(size_t)w * cfg.max_iters + q] = NAN;
         }
@@ -349,8 +375,8 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
       while (__any_sync(kFull, !done)) {
         const int nmax = group_max_i<DP>(done ? 0 : n);
         float dth;
-        bool finite;
-        const double lnl = eval_window<DP, true>(P, A, SQ, Gs, c, w, !done, nmax, th, ci, dth, finite);
+        bool finite, exact;
+        const double lnl = eval_window<DP, true>(P, A, SQ, Gs, c, w, !done, nmax, th, ci, dth, finite, exact);
         if (!done) {
           if (!finite) {
             st |= MDHP_ST_NONFINITE;
@@ -391,14 +417,15 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
       // lnL at the returned parameters (no gradient accumulation needed)
       const int nmax = group_max_i<DP>(n);
       float dth;
-      bool finite;
-      const double lnl = eval_window<DP, false>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite);
+      bool finite, exact;
+      const double lnl = eval_window<DP, false>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite, exact);
       if (slot < P.W) {
         if (live) store_params<DP>(A, c, D, w, th, theta, alpha, beta);
         if (c.j == 0) {
           lnl_out[w] = live ? lnl : (double)NAN;
           iters_out[w] = it;
-          status[w] = st0 | st;
+          status[w] = (st0 & kKeepStatus) | st;
+          if (exact) list_exact(xlist, xcount, w);
           if (trace && live)
             for (int q = it; q < cfg.max_iters; q++) trace[(size_t)w * cfg.max_iters + q] = NAN;
         }
@@ -412,7 +439,7 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
 template <int DP>
 static int launch_loglik_t(const Packed& P, const float* th, const float* al, const float* be,
                            double* lnl, float* gt, float* ga, float* gb, const int32_t* status,
-                           cudaStream_t st) {
+                           int32_t* xlist, int32_t* xcount, cudaStream_t st) {
   using SM = Smem<DP>;
   constexpr int WPB = 4;
   const size_t smem = WPB * SM::per_warp;
@@ -424,21 +451,22 @@ static int launch_loglik_t(const Packed& P, const float* th, const float* al, co
   }
   const int64_t units = (P.W + SM::G - 1) / SM::G;
   const unsigned blocks = (unsigned)((units + WPB - 1) / WPB);
-  kern<<<blocks, WPB * 32, smem, st>>>(P, th, al, be, lnl, gt, ga, gb, status);
+  kern<<<blocks, WPB * 32, smem, st>>>(P, th, al, be, lnl, gt, ga, gb, status, xlist, xcount);
   count_launch();
   return MDHP_OK;
 }
 
 int loglik_launch(const Packed& P, const float* th, const float* al, const float* be, double* lnl,
-                  float* gt, float* ga, float* gb, const int32_t* status, cudaStream_t st) {
+                  float* gt, float* ga, float* gb, const int32_t* status, int32_t* xlist,
+                  int32_t* xcount, cudaStream_t st) {
   if (P.W == 0) return MDHP_OK;
   switch (P.Dp) {
-    case 1: return launch_loglik_t<1>(P, th, al, be, lnl, gt, ga, gb, status, st);
-    case 2: return launch_loglik_t<2>(P, th, al, be, lnl, gt, ga, gb, status, st);
-    case 4: return launch_loglik_t<4>(P, th, al, be, lnl, gt, ga, gb, status, st);
-    case 8: return launch_loglik_t<8>(P, th, al, be, lnl, gt, ga, gb, status, st);
-    case 16: return launch_loglik_t<16>(P, th, al, be, lnl, gt, ga, gb, status, st);
-    case 32: return launch_loglik_t<32>(P, th, al, be, lnl, gt, ga, gb, status, st);
+    case 1: return launch_loglik_t<1>(P, th, al, be, lnl, gt, ga, gb, status, xlist, xcount, st);
+    case 2: return launch_loglik_t<2>(P, th, al, be, lnl, gt, ga, gb, status, xlist, xcount, st);
+    case 4: return launch_loglik_t<4>(P, th, al, be, lnl, gt, ga, gb, status, xlist, xcount, st);
+    case 8: return launch_loglik_t<8>(P, th, al, be, lnl, gt, ga, gb, status, xlist, xcount, st);
+    case 16: return launch_loglik_t<16>(P, th, al, be, lnl, gt, ga, gb, status, xlist, xcount, st);
+    case 32: return launch_loglik_t<32>(P, th, al, be, lnl, gt, ga, gb, status, xlist, xcount, st);
   }
   set_error("unsupported padded D %d", P.Dp);
   return MDHP_EDIM;
@@ -447,7 +475,7 @@ int loglik_launch(const Packed& P, const float* th, const float* al, const float
 template <int DP>
 static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float* al, float* be,
                         float* opt, double* lnl, int32_t* iters, int32_t* status, float* trace,
-                        int* counter, cudaStream_t st) {
+                        int* counter, int32_t* xlist, int32_t* xcount, cudaStream_t st) {
   using SM = Smem<DP>;
   constexpr int WPB = 4;
   const size_t smem = WPB * SM::per_warp;
@@ -470,22 +498,22 @@ static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float*
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
   kern<<<(unsigned)blocks, WPB * 32, smem, st>>>(P, cfg, th, al, be, opt, lnl, iters, status,
-                                                 trace, counter);
+                                                 trace, counter, xlist, xcount);
   count_launch();
   return MDHP_OK;
 }
 
 int fit_launch(const Packed& P, const FitCfgDev& cfg, float* th, float* al, float* be, float* opt,
                double* lnl, int32_t* iters, int32_t* status, float* trace, int* counter,
-               cudaStream_t st) {
+               int32_t* xlist, int32_t* xcount, cudaStream_t st) {
   if (P.W == 0) return MDHP_OK;
   switch (P.Dp) {
-    case 1: return launch_fit_t<1>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, st);
-    case 2: return launch_fit_t<2>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, st);
-    case 4: return launch_fit_t<4>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, st);
-    case 8: return launch_fit_t<8>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, st);
-    case 16: return launch_fit_t<16>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, st);
-    case 32: return launch_fit_t<32>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, st);
+    case 1: return launch_fit_t<1>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, xlist, xcount, st);
+    case 2: return launch_fit_t<2>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, xlist, xcount, st);
+    case 4: return launch_fit_t<4>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, xlist, xcount, st);
+    case 8: return launch_fit_t<8>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, xlist, xcount, st);
+    case 16: return launch_fit_t<16>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, xlist, xcount, st);
+    case 32: return launch_fit_t<32>(P, cfg, th, al, be, opt, lnl, iters, status, trace, counter, xlist, xcount, st);
   }
   set_error("unsupported padded D %d", P.Dp);
   return MDHP_EDIM;

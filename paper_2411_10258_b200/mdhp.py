@@ -89,6 +89,8 @@ def lib() -> ctypes.CDLL:
         L.mdhp_pack_windows.argtypes = [ctypes.POINTER(PackDesc), P, P, P, P, P, ctypes.c_size_t, P, P]
         L.mdhp_loglik_grad.restype = ctypes.c_int
         L.mdhp_loglik_grad.argtypes = [ctypes.POINTER(PackDesc), P, P, P, P, P, P, P, P, P, P]
+        L.mdhp_loglik_exact.restype = ctypes.c_int
+        L.mdhp_loglik_exact.argtypes = [ctypes.POINTER(PackDesc), P, P, P, P, P, P, P, P, P, P]
         L.mdhp_loglik_dense.restype = ctypes.c_int
         L.mdhp_loglik_dense.argtypes = [ctypes.POINTER(PackDesc), P, P, P, P, P, P, P]
         L.mdhp_hawkes_features.restype = ctypes.c_int
@@ -153,6 +155,19 @@ def _dev(x, dtype, name):
     if x.dtype != dtype or not x.is_contiguous():
         raise TypeError(f"{name} must be a contiguous {dtype} tensor")
     return x
+
+
+def _size(x, n, name):
+    """ValueError unless tensor x holds exactly n elements (the C side trusts the sizes)."""
+    if x is not None and x.numel() != n:
+        raise ValueError(f"{name} has {x.numel()} elements, expected {n}")
+    return x
+
+
+def _params(W, D, theta, alpha, beta):
+    for nm, x in (("theta", theta), ("alpha", alpha), ("beta", beta)):
+        _dev(x, torch.float32, nm)
+    _size(theta, W * D, "theta"); _size(alpha, W * D * D, "alpha"); _size(beta, W * D * D, "beta")
 
 
 def _stream(stream=None):
@@ -221,6 +236,7 @@ def pack_windows(D, t, mark, win_off, T, time_mode=TIME_RAW, eq6_lo=0.0, eq6_hi=
     _dev(t, torch.float64, "t"); _dev(mark, torch.int32, "mark")
     _dev(win_off, torch.int64, "win_off"); _dev(T, torch.float64, "T")
     W = T.numel(); E = t.numel()
+    _size(mark, E, "mark"); _size(win_off, W + 1, "win_off")
     desc = make_desc(D, W, E, time_mode, eq6_lo, eq6_hi, tie_policy)
     nb = packed_bytes(desc)
     if nb == 0:
@@ -236,11 +252,11 @@ def pack_windows(D, t, mark, win_off, T, time_mode=TIME_RAW, eq6_lo=0.0, eq6_hi=
     return Packed(desc, buf, status)
 
 
-def loglik_grad(pk: Packed, theta, alpha, beta, grads=True, out=None, stream=None):
-    """mdhp_loglik_grad.  theta f32[W,D], alpha/beta f32[W,D,D] (CUDA).  Returns dict of tensors."""
+def loglik_grad(pk: Packed, theta, alpha, beta, grads=True, out=None, stream=None, exact=False):
+    """mdhp_loglik_grad (exact=True: mdhp_loglik_exact, every window in fp64 on the GPU).
+    theta f32[W,D], alpha/beta f32[W,D,D] (CUDA).  Returns dict of tensors."""
     D, W = pk.D, pk.W
-    for nm, x in (("theta", theta), ("alpha", alpha), ("beta", beta)):
-        _dev(x, torch.float32, nm)
+    _params(W, D, theta, alpha, beta)
     dev = theta.device
     o = out or {}
     lnl = o.get("lnl") if o.get("lnl") is not None else torch.empty(W, dtype=torch.float64, device=dev)
@@ -249,18 +265,23 @@ def loglik_grad(pk: Packed, theta, alpha, beta, grads=True, out=None, stream=Non
         gt = o.get("g_theta") if o.get("g_theta") is not None else torch.empty(W, D, dtype=torch.float32, device=dev)
         ga = o.get("g_alpha") if o.get("g_alpha") is not None else torch.empty(W, D, D, dtype=torch.float32, device=dev)
         gb = o.get("g_beta") if o.get("g_beta") is not None else torch.empty(W, D, D, dtype=torch.float32, device=dev)
-    rc = lib().mdhp_loglik_grad(ctypes.byref(pk.desc), _ptr(pk.buf), _ptr(theta), _ptr(alpha),
-                                _ptr(beta), _ptr(lnl), _ptr(gt), _ptr(ga), _ptr(gb),
-                                _ptr(pk.status), _stream(stream))
-    _check(rc, "mdhp_loglik_grad")
+    _dev(lnl, torch.float64, "lnl"); _size(lnl, W, "lnl")
+    for nm, x, n in (("g_theta", gt, W * D), ("g_alpha", ga, W * D * D), ("g_beta", gb, W * D * D)):
+        if x is not None:
+            _dev(x, torch.float32, nm); _size(x, n, nm)
+    fn = lib().mdhp_loglik_exact if exact else lib().mdhp_loglik_grad
+    rc = fn(ctypes.byref(pk.desc), _ptr(pk.buf), _ptr(theta), _ptr(alpha),
+            _ptr(beta), _ptr(lnl), _ptr(gt), _ptr(ga), _ptr(gb),
+            _ptr(pk.status), _stream(stream))
+    _check(rc, "mdhp_loglik_exact" if exact else "mdhp_loglik_grad")
     return {"lnl": lnl, "g_theta": gt, "g_alpha": ga, "g_beta": gb}
 
 
 def loglik_dense(pk: Packed, theta, alpha, beta, out=None, stream=None):
     """mdhp_loglik_dense (ablation f3): lnL by the paper's all-pairs method.  -> lnL f64[W]."""
-    for nm, x in (("theta", theta), ("alpha", alpha), ("beta", beta)):
-        _dev(x, torch.float32, nm)
+    _params(pk.W, pk.D, theta, alpha, beta)
     lnl = out if out is not None else torch.empty(pk.W, dtype=torch.float64, device=theta.device)
+    _dev(lnl, torch.float64, "out"); _size(lnl, pk.W, "out")
     rc = lib().mdhp_loglik_dense(ctypes.byref(pk.desc), _ptr(pk.buf), _ptr(theta), _ptr(alpha), _ptr(beta),
                                  _ptr(lnl), _ptr(pk.status), _stream(stream))
     _check(rc, "mdhp_loglik_dense")
@@ -276,7 +297,10 @@ def hawkes_features(theta, alpha, beta, T_span, A, B, C, out=None, stream=None):
         _dev(x, torch.float32, nm)
     W, D = theta.shape[0], theta.shape[-1]
     H = A.shape[0]
+    _params(W, D, theta, alpha, beta)
+    _size(T_span, W, "T_span"); _size(A, H * D * D, "A"); _size(B, H * D * D, "B"); _size(C, H * D, "C")
     hks = out if out is not None else torch.empty(W, H, dtype=torch.float32, device=theta.device)
+    _dev(hks, torch.float32, "out"); _size(hks, W * H, "out")
     rc = lib().mdhp_hawkes_features(D, W, H, _ptr(theta), _ptr(alpha), _ptr(beta), _ptr(T_span),
                                     _ptr(A), _ptr(B), _ptr(C), _ptr(hks), _stream(stream))
     _check(rc, "mdhp_hawkes_features")
@@ -286,10 +310,10 @@ def hawkes_features(theta, alpha, beta, T_span, A, B, C, out=None, stream=None):
 def fit(pk: Packed, theta, alpha, beta, cfg: FitConfig, opt_state=None, trace=False, stream=None):
     """mdhp_fit.  theta/alpha/beta are updated IN PLACE (init in, fitted out)."""
     D, W = pk.D, pk.W
-    for nm, x in (("theta", theta), ("alpha", alpha), ("beta", beta)):
-        _dev(x, torch.float32, nm)
+    _params(W, D, theta, alpha, beta)
     if opt_state is not None:
         _dev(opt_state, torch.float32, "opt_state")
+        _size(opt_state, 2 * W * (D + 2 * D * D), "opt_state")
     dev = theta.device
     lnl = torch.empty(W, dtype=torch.float64, device=dev)
     iters = torch.empty(W, dtype=torch.int32, device=dev)
@@ -313,6 +337,8 @@ def fit_host(D, t, mark, win_off, T, theta, alpha, beta, cfg: FitConfig, time_mo
         if x.is_cuda or x.dtype != dt or not x.is_contiguous():
             raise TypeError(f"{nm} must be a contiguous CPU {dt} tensor")
     W = T.numel()
+    _size(mark, t.numel(), "mark"); _size(win_off, W + 1, "win_off")
+    _size(theta, W * D, "theta"); _size(alpha, W * D * D, "alpha"); _size(beta, W * D * D, "beta")
     desc = make_desc(D, W, t.numel(), time_mode, eq6_lo, eq6_hi, tie_policy)
     lnl = torch.empty(W, dtype=torch.float64)
     iters = torch.empty(W, dtype=torch.int32)
@@ -369,8 +395,7 @@ def seq_pack(D, t, mark, T, chunk_events=256, out: PackedSeq | None = None, t0=0
 
 def seq_loglik_grad(ps: PackedSeq, theta, alpha, beta, grads=True, stream=None):
     D = ps.D
-    for nm, x in (("theta", theta), ("alpha", alpha), ("beta", beta)):
-        _dev(x, torch.float32, nm)
+    _params(1, D, theta, alpha, beta)
     dev = theta.device
     lnl = torch.empty(1, dtype=torch.float64, device=dev)
     gt = torch.empty(D, dtype=torch.float32, device=dev) if grads else None
@@ -384,8 +409,11 @@ def seq_loglik_grad(ps: PackedSeq, theta, alpha, beta, grads=True, stream=None):
 
 def seq_fit(ps: PackedSeq, theta, alpha, beta, cfg: FitConfig, opt_state=None, trace=False, stream=None):
     """mdhp_seq_fit; theta [D], alpha/beta [D,D] fp32 CUDA tensors updated in place."""
-    for nm, x in (("theta", theta), ("alpha", alpha), ("beta", beta)):
-        _dev(x, torch.float32, nm)
+    D = ps.D
+    _params(1, D, theta, alpha, beta)
+    if opt_state is not None:
+        _dev(opt_state, torch.float32, "opt_state")
+        _size(opt_state, 2 * (D + 2 * D * D), "opt_state")
     dev = theta.device
     lnl = torch.empty(1, dtype=torch.float64, device=dev)
     iters = torch.empty(1, dtype=torch.int32, device=dev)

@@ -97,12 +97,3 @@ def assert_grad_close(got, ref, scale, rel=1e-3, gross_rel=1e-4, what=""):
         raise AssertionError(f"{what}: {bad.sum()} entries out of tolerance, e.g. "
                              + "; ".join(f"{tuple(i)} got {got[tuple(i)]:.9g} ref {ref[tuple(i)]:.9g} "
                                          f"scale {np.broadcast_to(scale, ref.shape)[tuple(i)]:.3g}" for i in idx))
-
-
-def lnl_tol(ref, rel=1e-4):
-    """DESIGN.md R17: |d lnL| <= 1e-4 |lnL_ref|, except where lnL_ref is a
-    cancellation of much larger terms (|lnL_ref| < 1e-2 gross, gross = |sum ln lambda| + Gamma =
-    |lnL + Gamma| + Gamma): there fp32 rounding of the terms is bounded by the gross scale, and the
-    bar is 1e-6 gross (continuous with the relative bar at the boundary)."""
-    gross = abs(ref["lnl"] + ref["gamma"]) + abs(ref["gamma"])
-    return rel * max(abs(ref["lnl"]), 1e-2 * gross)

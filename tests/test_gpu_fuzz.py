@@ -1,5 +1,7 @@
 """Randomised GPU parity sweep over EVERY D in 1..32 (each padded width DP and each D < DP
-padding case), against the fp64 oracle on the same seeded inputs (R17 bars).
+padding case), against the fp64 oracle on the same seeded inputs: lnL within the plain 1e-4
+relative bar of north_star on every window (R24: windows whose fp32 value could miss
+it are re-evaluated in fp64 on the GPU), gradients within R17.
 
 Windows are drawn to stress the layout rather than to look like traffic: lengths 0, 1, 2, a few
 hundred, and an occasional long window among short ones (ragged warps, long-first order);
@@ -71,7 +73,7 @@ def test_fuzz_loglik_all_D(D):
         a, z = b["win_off"][w], b["win_off"][w + 1]
         p = (f32(th[w]).astype(float), f32(al[w]).astype(float), f32(be[w]).astype(float))
         ref = oracle.loglik_rec(D, t32[a:z], b["mark"][a:z], T32[w], *p)
-        assert abs(out["lnl"][w] - ref["lnl"]) <= H.lnl_tol(ref), (D, w, z - a, out["lnl"][w], ref["lnl"])
+        assert abs(out["lnl"][w] - ref["lnl"]) <= 1e-4 * abs(ref["lnl"]), (D, w, z - a, out["lnl"][w], ref["lnl"])
         sth, sal, sbe = H.grad_scales(t32[a:z], b["mark"][a:z], T32[w], *p, ref)
         H.assert_grad_close(out["g_theta"][w], ref["g_theta"], sth, what=f"D{D} w{w} theta")
         H.assert_grad_close(out["g_alpha"][w], ref["g_alpha"], sal, what=f"D{D} w{w} alpha")
@@ -130,7 +132,7 @@ def test_fuzz_sequence_path(D, ce):
     out = {k: v.cpu().numpy() for k, v in r.items() if v is not None}
     prm = (f32(th).astype(float), f32(al).astype(float), f32(be).astype(float))
     ref = oracle.loglik_rec(D, t, m, T, *prm)
-    assert abs(out["lnl"][0] - ref["lnl"]) <= H.lnl_tol(ref), (D, ce, out["lnl"][0], ref["lnl"])
+    assert abs(out["lnl"][0] - ref["lnl"]) <= 1e-4 * abs(ref["lnl"]), (D, ce, out["lnl"][0], ref["lnl"])
     sth, sal, sbe = H.grad_scales(t, m, T, *prm, ref)
     H.assert_grad_close(out["g_theta"], ref["g_theta"], sth, what=f"seq D{D} theta")
     H.assert_grad_close(out["g_alpha"], ref["g_alpha"], sal, what=f"seq D{D} alpha")
@@ -157,25 +159,72 @@ def test_chunk_hint_is_a_valid_chunk_size():
     assert lnl[0] == pytest.approx(lnl[1], rel=1e-5) and lnl[2] == lnl[0]
 
 
-def test_fuzz_cancellation_windows_found_by_the_sweep():
-    """The two windows of tools/fuzz_sweep.py (400 batches, 7,871 windows) whose lnL is a
-    cancellation of much larger terms (lnL ~ 0.03-0.05 against a gross scale ~1e2): beyond the
-    plain 1e-4 relative bar, within R17's gross-scale bar."""
-    for k, D, w in ((268, 12, 22), (337, 11, 16)):
-        rng = np.random.default_rng(50000 + k)
-        assert int(rng.integers(1, 33)) == D
-        W = int(rng.integers(1, 40))
-        b = fuzz_windows(rng, D, W)
-        th, al, be = fuzz_params(rng, W, D)
-        dev = (torch.tensor(b["t"], dtype=torch.float64, device=DEV), torch.tensor(b["mark"], dtype=torch.int32, device=DEV),
-               torch.tensor(b["win_off"], dtype=torch.int64, device=DEV), torch.tensor(b["T"], dtype=torch.float64, device=DEV))
-        pk = M.pack_windows(D, *dev)
-        r = M.loglik_grad(pk, *(torch.tensor(f32(x), device=DEV) for x in (th, al, be)), grads=False)
-        got = float(r["lnl"][w])
-        t32, T32, _ = H.oracle_times(b, D)
+# (batch, D, window) of tools/fuzz_sweep.py whose lnL is a cancellation of much larger terms
+# (lnL ~ 0.02-0.85 against sum |ln lambda| + Gamma ~ 1e2): the round-1 fp32 path missed the
+# plain 1e-4 bar on exactly these (profiles/r01_fuzz_sweep_1000.txt)
+SWEEP_CANCELLATION = ((268, 12, 22), (337, 11, 16), (410, 10, 4), (763, 8, 7))
+
+
+def _sweep_batch(k, D):
+    rng = np.random.default_rng(50000 + k)
+    assert int(rng.integers(1, 33)) == D
+    W = int(rng.integers(1, 40))
+    b = fuzz_windows(rng, D, W)
+    th, al, be = fuzz_params(rng, W, D)
+    return b, th, al, be
+
+
+@pytest.mark.parametrize("k,D,w", SWEEP_CANCELLATION)
+def test_fuzz_cancellation_windows_plain_bar(k, D, w):
+    """The sweep's cancellation windows meet the plain 1e-4 relative lnL bar (and the gradients
+    R17) through mdhp_loglik_grad, and the fit's final lnL at the same parameters (max_iters 0)
+    meets it too: the fp64 re-evaluation (exact.cu) is taken for them."""
+    b, th, al, be = _sweep_batch(k, D)
+    dev = (torch.tensor(b["t"], dtype=torch.float64, device=DEV), torch.tensor(b["mark"], dtype=torch.int32, device=DEV),
+           torch.tensor(b["win_off"], dtype=torch.int64, device=DEV), torch.tensor(b["T"], dtype=torch.float64, device=DEV))
+    pk = M.pack_windows(D, *dev)
+    tt = [torch.tensor(f32(x), device=DEV) for x in (th, al, be)]
+    r = M.loglik_grad(pk, *tt)
+    fr = M.fit(pk, *(x.clone() for x in tt), M.FitConfig(max_iters=0, tol_rel=0.0))
+    torch.cuda.synchronize()
+    t32, T32, _ = H.oracle_times(b, D)
+    a, z = b["win_off"][w], b["win_off"][w + 1]
+    p = (f32(th[w]).astype(float), f32(al[w]).astype(float), f32(be[w]).astype(float))
+    ref = oracle.loglik_rec(D, t32[a:z], b["mark"][a:z], T32[w], *p)
+    gross = abs(ref["lnl"] + ref["gamma"]) + abs(ref["gamma"])
+    assert abs(ref["lnl"]) < 1e-2 * gross          # the cancellation regime
+    for got in (float(r["lnl"][w]), float(fr["lnl"][w])):
+        assert abs(got - ref["lnl"]) <= 1e-4 * abs(ref["lnl"]), (k, w, got, ref["lnl"], gross)
+    sth, sal, sbe = H.grad_scales(t32[a:z], b["mark"][a:z], T32[w], *p, ref)
+    H.assert_grad_close(r["g_theta"][w].cpu().numpy(), ref["g_theta"], sth, what="theta")
+    H.assert_grad_close(r["g_alpha"][w].cpu().numpy(), ref["g_alpha"], sal, what="alpha")
+    H.assert_grad_close(r["g_beta"][w].cpu().numpy(), ref["g_beta"], sbe, what="beta")
+
+
+@pytest.mark.parametrize("D", [1, 2, 5, 8, 13, 16, 24, 32])
+def test_exact_kernel_vs_oracle(D):
+    """mdhp_loglik_exact (every window in fp64 on the GPU) against the fp64 oracle on fuzzed
+    batches: lnL within 1e-9 relative (or 1e-9 of the gross scale), gradients within 1e-7 of
+    R17's gross scale -- an fp64 evaluation, so far below the fp32 bars."""
+    rng = np.random.default_rng(9400 + D)
+    W = int(rng.integers(5, 20))
+    b = fuzz_windows(rng, D, W)
+    th, al, be = fuzz_params(rng, W, D)
+    dev = (torch.tensor(b["t"], dtype=torch.float64, device=DEV), torch.tensor(b["mark"], dtype=torch.int32, device=DEV),
+           torch.tensor(b["win_off"], dtype=torch.int64, device=DEV), torch.tensor(b["T"], dtype=torch.float64, device=DEV))
+    pk = M.pack_windows(D, *dev)
+    r = M.loglik_grad(pk, *(torch.tensor(f32(x), device=DEV) for x in (th, al, be)), exact=True)
+    torch.cuda.synchronize()
+    out = {k: v.cpu().numpy() for k, v in r.items() if v is not None}
+    t32, T32, _ = H.oracle_times(b, D)
+    for w in range(W):
         a, z = b["win_off"][w], b["win_off"][w + 1]
-        ref = oracle.loglik_rec(D, t32[a:z], b["mark"][a:z], T32[w], f32(th[w]).astype(float),
-                                f32(al[w]).astype(float), f32(be[w]).astype(float), grads=False)
+        p = (f32(th[w]).astype(float), f32(al[w]).astype(float), f32(be[w]).astype(float))
+        ref = oracle.loglik_rec(D, t32[a:z], b["mark"][a:z], T32[w], *p)
         gross = abs(ref["lnl"] + ref["gamma"]) + abs(ref["gamma"])
-        assert abs(ref["lnl"]) < 1e-2 * gross          # the cancellation regime of R17
-        assert abs(got - ref["lnl"]) <= H.lnl_tol(ref), (k, w, got, ref["lnl"], gross)
+        assert abs(out["lnl"][w] - ref["lnl"]) <= 1e-9 * max(abs(ref["lnl"]), gross), (D, w)
+        sth, sal, sbe = H.grad_scales(t32[a:z], b["mark"][a:z], T32[w], *p, ref)
+        # fp32 outputs: one rounding of the fp64 result
+        H.assert_grad_close(out["g_theta"][w], ref["g_theta"], sth, rel=2e-7, gross_rel=1e-7, what="theta")
+        H.assert_grad_close(out["g_alpha"][w], ref["g_alpha"], sal, rel=2e-7, gross_rel=1e-7, what="alpha")
+        H.assert_grad_close(out["g_beta"][w], ref["g_beta"], sbe, rel=2e-7, gross_rel=1e-7, what="beta")

@@ -275,6 +275,32 @@ def test_fit_convergence_and_status():
         assert abs(g["lnl"][w] - o[w]["lnl"]) <= 1e-4 * max(abs(o[w]["lnl"]), 1.0)
 
 
+@pytest.mark.parametrize("tol", [1e-6, 0.0])
+def test_fit_status_not_carried_over_between_calls(tol):
+    """A second mdhp_fit on the same packed batch reports only its own outcome: CONVERGED
+    (or NONFINITE / DIVERGED) bits of an earlier call are dropped, validation bits are kept
+    (include/mdhp.h mdhp_fit, win_status)."""
+    D = 3
+    b, _ = H.small_batch(D, 6, seed=500, edges=True)
+    W = len(b["T"])
+    pk = M.pack_windows(D, *dev_batch(b))
+    st_pack = pk.status.cpu().numpy()[:W].copy()
+    th = torch.full((W, D), 2.0, device=DEV); al = torch.full((W, D, D), 10.0, device=DEV)
+    be = torch.full((W, D, D), 20.0, device=DEV)
+    M.fit(pk, th, al, be, M.FitConfig(max_iters=2000, lr=0.05, tol_rel=1e-6, patience=10))
+    torch.cuda.synchronize()
+    st1 = pk.status.cpu().numpy()[:W].copy()
+    assert (st1 & mdhp.ST_CONVERGED).any()
+    th = torch.full((W, D), 2.0, device=DEV); al = torch.full((W, D, D), 10.0, device=DEV)
+    be = torch.full((W, D, D), 20.0, device=DEV)
+    M.fit(pk, th, al, be, M.FitConfig(max_iters=3, lr=0.05, tol_rel=tol, patience=10))
+    torch.cuda.synchronize()
+    st2 = pk.status.cpu().numpy()[:W]
+    keep = mdhp.ST_INVALID | mdhp.ST_EMPTY
+    assert not (st2 & (mdhp.ST_CONVERGED | mdhp.ST_DIVERGED)).any(), st2
+    np.testing.assert_array_equal(st2 & keep, st_pack & keep)
+
+
 def test_fit_host_end_to_end():
     """mdhp_fit_host (host buffers, copies inside) equals pack + fit on device buffers."""
     D = 4
@@ -458,3 +484,25 @@ def test_converged_mode_refill_is_batch_invariant():
                   be0[w:w + 1])
         for k in range(6):
             np.testing.assert_array_equal(one[k][0], full[k][w], err_msg=f"window {w} output {k}")
+
+
+def test_wrappers_reject_mismatched_sizes():
+    """The binding checks every buffer size before calling the C side (which trusts them)."""
+    D = 4
+    b, _ = H.small_batch(D, 3, seed=1, edges=False)
+    W = len(b["T"])
+    t, m, off, T = dev_batch(b)
+    with pytest.raises(ValueError):
+        M.pack_windows(D, t, m, off[:-1].contiguous(), T)
+    pk = M.pack_windows(D, t, m, off, T)
+    th = torch.ones(W, D, device=DEV); al = torch.ones(W, D, D, device=DEV); be = torch.ones(W, D, D, device=DEV)
+    for bad in ((th[:-1].contiguous(), al, be), (th, al[:-1].contiguous(), be), (th, al, be[:, :-1].contiguous())):
+        with pytest.raises(ValueError):
+            M.loglik_grad(pk, *bad)
+        with pytest.raises(ValueError):
+            M.fit(pk, *(x.clone() for x in bad), M.FitConfig(max_iters=1))
+    with pytest.raises(ValueError):
+        M.fit(pk, th, al, be, M.FitConfig(max_iters=1), opt_state=torch.zeros(W, 3, device=DEV))
+    with pytest.raises(ValueError):
+        M.fit_host(D, t.cpu(), m.cpu(), off.cpu(), T.cpu(), th.cpu()[:-1].contiguous(), al.cpu(), be.cpu(),
+                   M.FitConfig(max_iters=1))

@@ -1,7 +1,8 @@
 """Extended randomised parity sweep (evidence run, not part of the test suite): N random batches
 (D uniform in 1..32, ragged/empty/long windows, ties, events at 0 and T, random parameters) through
-mdhp_pack_windows + mdhp_loglik_grad vs the fp64 oracle; prints the worst relative lnL error and
-the worst gradient error in units of the R17 tolerance.  usage: python tools/fuzz_sweep.py [N]"""
+mdhp_pack_windows + mdhp_loglik_grad vs the fp64 oracle; prints the number of windows over the
+plain 1e-4 relative lnL bar, the worst relative lnL error and the worst gradient error in units
+of the R17 tolerance.  usage: python tools/fuzz_sweep.py [N]"""
 import os
 import sys
 
@@ -21,7 +22,7 @@ def grad_ratio(got, ref, scale, rel=1e-3, gross_rel=1e-4):
 
 
 def main(n):
-    worst_lnl, worst_g, worst_r17, windows, events = 0.0, 0.0, 0.0, 0, 0
+    worst_lnl, worst_g, windows, events, bad = 0.0, 0.0, 0, 0, 0
     for k in range(n):
         rng = np.random.default_rng(50000 + k)
         D = int(rng.integers(1, 33))
@@ -41,8 +42,8 @@ def main(n):
             p = (f32(th[w]).astype(float), f32(al[w]).astype(float), f32(be[w]).astype(float))
             ref = oracle.loglik_rec(D, t32[a:z], b["mark"][a:z], T32[w], *p)
             e = abs(out["lnl"][w] - ref["lnl"]) / max(abs(ref["lnl"]), 1e-300)
-            worst_r17 = max(worst_r17, abs(out["lnl"][w] - ref["lnl"]) / H.lnl_tol(ref))
             if e > 1e-4:
+                bad += 1
                 print(f"  lnL out of bar: batch {k} D={D} window {w} n={z - a} T={T32[w]} "
                       f"gpu={out['lnl'][w]!r} oracle={ref['lnl']!r} rel={e:.3g} "
                       f"sum|ln lambda| scale: N={z - a}", flush=True)
@@ -53,10 +54,10 @@ def main(n):
                           grad_ratio(out["g_beta"][w], ref["g_beta"], sbe))
             windows += 1
             events += z - a
-    print(f"{n} batches, {windows} windows, {events} events: worst lnL rel err {worst_lnl:.3g} "
-          f"(plain bar 1e-4), worst lnL error {worst_r17:.3g} x the R17 tolerance (bar 1), "
+    print(f"{n} batches, {windows} windows, {events} events: {bad} windows over the plain lnL bar, "
+          f"worst lnL rel err {worst_lnl:.3g} (bar 1e-4), "
           f"worst gradient error {worst_g:.3g} x the R17 tolerance (bar 1)")
-    return 0 if worst_r17 <= 1.0 and worst_g <= 1.0 else 1
+    return 0 if worst_lnl <= 1e-4 and worst_g <= 1.0 else 1
 
 
 
