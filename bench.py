@@ -2,12 +2,19 @@
 """MDHP-GDS benchmark (BASELINE.json metric: event·iterations/sec and windows fitted/sec).
 
 One step = the whole hot path over one batch resident in HBM: mdhp_pack_windows (a1) +
-mdhp_fit with a fixed iteration count (a2-a6, one persistent kernel) + (N > 1) the final NCCL
-gather of the per-window records to rank 0 (a8).  Workload (N = 1, per GPU; weak scaling):
-BASELINE config 5 — 1,048,576 windows, D = 16 message IDs, ~1,024 events/window, T = 1 s,
-Adam lr 0.05 from the SPEC init (alpha 0.5, beta 1, theta 0.1), 500 iterations.
+mdhp_fit with a fixed iteration count (a2-a6, one persistent kernel, + the fp64 re-evaluation
+of cancellation windows) + (N > 1) the final NCCL gather of the per-window records to rank 0
+and their reassembly in global window order (a8).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+Headline workload: BASELINE config 5 — ONE batch of 1,048,576 windows, D = 16 message IDs,
+~1,024 events/window, T = 1 s, Adam lr 0.05 from the SPEC init (alpha 0.5, beta 1, theta 0.1;
+S:182-183), 500 iterations.  At N GPUs the batch is cut into N contiguous window ranges with
+equal event totals (shard.balanced_ranges on the event prefix sums): STRONG scaling (SURVEY
+8(e)); --weak gives every rank its own 1,048,576 windows instead.  At N = 1 the line also carries
+one-step sub-results for the other BASELINE configs (cfg1-cfg4) and cfg5 in converged mode, each
+with its roofline fraction and lnL parity against the fp64 oracle.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--weak]
   torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
 
 Prints ONE JSON line on rank 0.  See DESIGN.md section 6 for every field.
@@ -15,6 +22,7 @@ Prints ONE JSON line on rank 0.  See DESIGN.md section 6 for every field.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -29,6 +37,9 @@ sys.path.insert(0, ROOT)
 METRIC = "MDHP-GDS event·iterations/sec and windows fitted/sec at 1/2/4/8 B200"
 UNIT = "event·iterations/s"
 MUFU_PEAK_GOPS = 148 * 16 * 1.965  # 148 SMs x 16 MUFU ops/clk x 1.965 GHz
+MIO_PEAK_GSLOTS = 148 * 1.965      # one shared-wavefront-or-shuffle slot per clock per SM
+KERNEL_SOURCES = ("common.cuh", "eval.cuh", "fit.cu", "exact.cu")
+CAPTURE = os.path.join(ROOT, "profiles", "r02_k_fit_capture.json")
 
 
 def parse():
@@ -38,10 +49,14 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg5")
-    ap.add_argument("--windows", type=int, default=None, help="windows per GPU (default: config)")
+    ap.add_argument("--windows", type=int, default=None, help="windows in the batch (default: config)")
     ap.add_argument("--iters", type=int, default=500)
+    ap.add_argument("--weak", action="store_true",
+                    help="N > 1: every rank fits its own full batch (weak scaling) instead of a share "
+                         "of one batch (strong scaling, the default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the per-config sub-results (N = 1)")
     ap.add_argument("--cpu-windows", type=int, default=None)
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--inject", default="none", choices=["none", "PLA", "DEA", "ASA", "DAM"],
@@ -60,13 +75,36 @@ def parse():
 
 
 WORKLOADS = {
-    # name: (recipe key, windows per GPU)
+    # name: (recipe key, windows in the batch)
+    "cfg1": ("cfg1", 1),
     "cfg2": ("cfg2", 4096),
     "cfg3": ("cfg3", 65536),
     "cfg4": ("cfg4", 1),
     "cfg5": ("cfg5", 1 << 20),
     "feat": ("cfg5", 1 << 20),   # row f4: Hawkes-gate features of cfg5-sized fitted parameters
 }
+
+
+def source_hash():
+    """Hash of the k_fit sources: a committed ncu capture is used only for the kernel it measured."""
+    h = hashlib.sha256()
+    for f in KERNEL_SOURCES:
+        with open(os.path.join(ROOT, "paper_2411_10258_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def kernel_capture(W, E, evals):
+    """The committed ncu capture of this exact k_fit launch (profiles/r02_k_fit_capture.json), or
+    None if the kernel sources or the launch differ from the captured ones."""
+    if not os.path.exists(CAPTURE):
+        return None
+    cj = json.load(open(CAPTURE))
+    if cj.get("source_hash") != source_hash():
+        return None
+    if cj.get("windows") != W or cj.get("events") != E or cj.get("evaluations") != evals:
+        return None
+    return cj
 
 
 def bench_loglik(args, rc, b, W, world, rank, dev):
@@ -220,74 +258,158 @@ def bench_seq_sharded(args, rc, world, rank, dev):
     return 0
 
 
-def bench_seq(args, rc, world, rank, dev):
-    """--config cfg4: one long sequence per GPU (replicas at N > 1: the sequence path does not
-    shard, DESIGN.md section 7), fitted by the chunked-scan path (mdhp_seq_fit)."""
+def fit_cfg_for(M, name, iters, tol):
+    """The fit each config is quoted on: cfg1 500 plain GD iterations on the mean loss (SURVEY
+    8(d)); the others Adam lr 0.05, fixed iterations or converged mode."""
+    if name == "cfg1":
+        return M.FitConfig(max_iters=iters, optimizer="gd", lr=0.5, loss="mean", tol_rel=tol, patience=10)
+    return M.FitConfig(max_iters=iters, optimizer="adam", lr=0.05, tol_rel=tol, patience=10)
+
+
+def gen_batch(rc, name, W, seed, first, dev):
+    from synth import gen
+    from synth import gpu as sgpu
+    import torch
+    params = None
+    if name == "cfg1":   # BASELINE cfg1 / SURVEY 8(d): fixed generating parameters
+        params = {k: torch.tensor(v, dtype=torch.float32).expand((W,) + v.shape).contiguous()
+                  for k, v in gen.CFG1_PARAMS.items()}
+    return sgpu.make_batch_gpu(rc, W, seed=seed, first_window=first, device=dev, params=params)
+
+
+def run_windows(M, rc, name, W_total, cfg, world, rank, dev, steps, warmup, strong, seed,
+                clocks=None, keep=False):
+    """Pack + fit of one batch of windows (config `name`), timed over `steps` steps after
+    `warmup` untimed ones; strong: the ranks share one batch (balanced_ranges), weak: each
+    rank fits its own W_total windows.  Returns the measurements (and the rank's data if keep)."""
+    import numpy as np
     import torch
     import torch.distributed as dist
-    import paper_2411_10258_b200 as M
-    from synth import gpu as sgpu
+    from paper_2411_10258_b200 import shard
     D = rc.D
-    if args.shard_seq:
-        return bench_seq_sharded(args, rc, world, rank, dev)
-    b = sgpu.make_batch_gpu(rc, 1, seed=args.seed, first_window=rank, device=dev)
-    N = int(b["win_off"][-1])
-    ce = args.chunk or M.seq_chunk_hint(D, N)
-    ps = M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=ce)
-    th0 = b["theta"][0].clone(); al0 = b["alpha"][0].clone(); be0 = b["beta"][0].clone()
-    th, al, be = th0.clone(), al0.clone(), be0.clone()
-    cfg = M.FitConfig(max_iters=args.iters, optimizer="adam", lr=0.05, tol_rel=0.0)
+    if strong:
+        b = gen_batch(rc, name, W_total, seed, 0, dev)
+        counts = (b["win_off"][1:] - b["win_off"][:-1]).cpu().numpy()
+        ranges = shard.balanced_ranges(counts, world)
+    else:
+        b = gen_batch(rc, name, W_total, seed, rank * W_total, dev)
+        ranges = [(r * W_total, (r + 1) * W_total) for r in range(world)]
+    lo, hi = ranges[rank]
+    if strong:
+        t, m, off, T = shard.slice_csr(b["t"], b["mark"], b["win_off"], b["T"], lo, hi)
+    else:
+        t, m, off, T = b["t"], b["mark"], b["win_off"], b["T"]
+    t, m, off, T = t.contiguous(), m.contiguous(), off.contiguous(), T.contiguous()
+    del b
+    n = hi - lo
+    n_max = max(z - a for a, z in ranges)
+    E = int(off[-1])
+    init_th = torch.full((n, D), 0.1, device=dev)
+    init_al = torch.full((n, D, D), 0.5, device=dev)
+    init_be = torch.full((n, D, D), 1.0, device=dev)
+    th, al, be = init_th.clone(), init_al.clone(), init_be.clone()
+    rec = torch.zeros(n_max, shard.record_width(D), dtype=torch.float32, device=dev)
+    gathered = [torch.empty_like(rec) for _ in range(world)] if (world > 1 and rank == 0) else None
     stream = torch.cuda.current_stream()
+    packed = None
+    out = {}
 
-    def step():
-        th.copy_(th0); al.copy_(al0); be.copy_(be0)
-        M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=ce, out=ps)
-        return M.seq_fit(ps, th, al, be, cfg)
-    for _ in range(max(args.warmup, 1)):
+    def step(ev=None):
+        nonlocal packed
+        th.copy_(init_th); al.copy_(init_al); be.copy_(init_be)
+        packed = M.pack_windows(D, t, m, off, T, time_mode=1, out=packed)
+        if ev is not None:
+            ev[0].record(stream)
+        r = M.fit(packed, th, al, be, cfg)
+        if ev is not None:
+            ev[1].record(stream)
+        if world > 1:   # a8: one gather of fixed-size per-window records to rank 0, reassembly
+            out["global"] = shard.gather_step(th, al, be, r["lnl"], r["iters"], r["status"], rec, ranges,
+                                              world, rank, gathered=gathered)
+        return r
+
+    for _ in range(max(warmup, 1)):   # at least one: the iteration counts come from it
         r = step()
     torch.cuda.synchronize()
-    evals = int(r["iters"][0]) + 1
+    cnt = (off[1:] - off[:-1])
+    iters_run = r["iters"].to(torch.int64)
+    ev_it = int((cnt * iters_run).sum())               # event-iterations (optimizer steps)
+    ev_eval = int((cnt * (iters_run + 1)).sum())       # event-evaluations (+ the final lnL)
     if world > 1:
         dist.barrier()
+    torch.cuda.synchronize()
+    if clocks is not None:
+        clocks.start()
     L0 = M.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fit_ev = []
     e0.record(stream)
-    for _ in range(args.steps):
-        r = step()
+    for _ in range(steps):
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        r = step(ev)
+        fit_ev.append(ev)
     e1.record(stream)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if clocks is not None else None
+    launches = M.launch_count() - L0
     ms = e0.elapsed_time(e1)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    fit_ms = sum(a.elapsed_time(z) for a, z in fit_ev) / steps
+    per = torch.tensor([ms, fit_ms, float(ev_it), float(ev_eval), float(n), float(E)], dtype=torch.float64,
+                       device=dev)
     if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    value = world * N * evals * args.steps / (float(t_max) / 1e3)
-    if rank == 0:
-        print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                          "warmup": args.warmup, "ms_per_step": float(t_max) / args.steps,
-                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                          "data": f"synthetic (Ogata-thinned MDHP on GPU, recipe cfg4, seed {args.seed})",
-                          "config": {"workload": f"cfg4: one sequence/GPU, D={D}, {N} events over {rc.T}s, "
-                                                 f"chunked scan ({ce} events/chunk{'' if args.chunk else ', mdhp_seq_chunk_hint'}), Adam lr 0.05, {args.iters} "
-                                                 "fixed iterations + final eval", "events": N},
-                          "gpu_launches": int(M.launch_count() - L0)}), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-    return 0
+        allp = [torch.empty_like(per) for _ in range(world)]
+        dist.all_gather(allp, per)
+    else:
+        allp = [per]
+    allp = torch.stack(allp).cpu().numpy()
+    ms_max = float(allp[:, 0].max())
+    tot_ev_it, tot_eval, tot_w = float(allp[:, 2].sum()), float(allp[:, 3].sum()), float(allp[:, 4].sum())
+    res = {
+        "value": tot_ev_it * steps / (ms_max / 1e3), "ms_per_step": ms_max / steps,
+        "windows_fitted_per_s": tot_w * steps / (ms_max / 1e3),
+        "fit_ms": fit_ms, "fit_ms_max_over_ranks": float(allp[:, 1].max()),
+        "ev_it_per_step": tot_ev_it, "ev_eval_per_step": tot_eval,
+        "local_ev_eval": ev_eval, "local_E": E, "local_W": n,
+        "mean_iters": float(iters_run.double().mean()) if n else 0.0,
+        "launches": int(launches), "clocks": clk, "ranges": ranges,
+        "per_rank": {"windows": [int(x) for x in allp[:, 4]], "events": [int(x) for x in allp[:, 5]],
+                     "fit_ms": [round(float(x), 3) for x in allp[:, 1]],
+                     "step_ms": [round(float(x) / steps, 3) for x in allp[:, 0]]},
+    }
+    res["imbalance"] = float(allp[:, 1].max() / max(allp[:, 1].mean(), 1e-9))
+    if keep:
+        res["data"] = {"t": t, "mark": m, "win_off": off, "T": T, "theta": th, "alpha": al, "beta": be,
+                       "lnl": r["lnl"], "iters": r["iters"], "status": r["status"],
+                       "init": (init_th, init_al, init_be)}
+    return res
 
 
-def run_e2e(M, b, D, W, cfg, init_th, init_al, init_be, ev_it_per_step, world, dev):
-    """e2e: the same metric through mdhp_fit_host on pinned host buffers (H2D of the CSR and the
-    init, pack, fit, D2H of the results inside the timed call), after one untimed warm-up call.
-    If a rank cannot pin its host buffers (host memory at N = 8), every rank reports the reason
-    instead of the number (agreed by an all-reduce, so no rank waits in a barrier alone)."""
+def roofline_of(D, ev_eval, fit_ms, kernel):
+    """MUFU roofline of k_fit: 2D+2 MUFU ops per event-evaluation over the fit
+    kernel's CUDA-event time, against 148 SMs x 16/clk x clocks.max.sm."""
+    Dp = 1 << (D - 1).bit_length()
+    ach = ev_eval * (2 * D + 2) / (fit_ms / 1e3) / 1e9
+    return {"bound": "alu", "achieved": ach, "peak": MUFU_PEAK_GOPS, "unit": "Gop/s (MUFU)",
+            "frac": ach / MUFU_PEAK_GOPS, "kernel": f"{kernel}<{Dp}>",
+            "per_unit": f"{2 * D + 2} MUFU ops per event-evaluation (2D ex2 + lg2 + rcp)"}
+
+
+def run_e2e(M, res, D, cfg, world, dev, calls=3):
+    """e2e: the same metric through mdhp_fit_host on pinned host buffers (H2D of this rank's CSR
+    share and the init, pack, fit, D2H of the results inside each timed call), mean of `calls`
+    timed calls after one untimed warm-up call, max over ranks.  If a rank cannot pin its host
+    buffers, every rank reports the reason instead (agreed by an all-reduce)."""
     import torch
     import torch.distributed as dist
+    d = res["data"]
     err = None
     try:
-        t_h = b["t"].cpu().pin_memory(); m_h = b["mark"].cpu().pin_memory()
-        o_h = b["win_off"].cpu().pin_memory(); T_h = b["T"].cpu().pin_memory()
-        th_h = init_th.cpu().pin_memory(); al_h = init_al.cpu().pin_memory(); be_h = init_be.cpu().pin_memory()
-        ths, als, bes = th_h.clone().pin_memory(), al_h.clone().pin_memory(), be_h.clone().pin_memory()
+        t_h = d["t"].cpu().pin_memory(); m_h = d["mark"].cpu().pin_memory()
+        o_h = d["win_off"].cpu().pin_memory(); T_h = d["T"].cpu().pin_memory()
+        th0, al0, be0 = (x.cpu().pin_memory() for x in d["init"])
+        ths, als, bes = th0.clone().pin_memory(), al0.clone().pin_memory(), be0.clone().pin_memory()
     except (RuntimeError, MemoryError) as ex:
         err = f"{type(ex).__name__}: {str(ex)[:200]}"
     ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=dev)
@@ -295,25 +417,61 @@ def run_e2e(M, b, D, W, cfg, init_th, init_al, init_be, ev_it_per_step, world, d
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     if int(ok[0]) == 0:
         return {"value": None, "unit": UNIT, "error": err or "another rank could not pin its host buffers"}
-    bi = sum(x.numel() * x.element_size() for x in (t_h, m_h, o_h, T_h, th_h, al_h, be_h))
-    bo = (th_h.numel() + al_h.numel() + be_h.numel()) * 4 + W * (8 + 4 + 4)
-    ke = 1   # one untimed warm-up call (workspace pool), then ke timed calls
-    M.fit_host(D, t_h, m_h, o_h, T_h, ths, als, bes, cfg, time_mode=1)
-    dt = 0.0
-    for _ in range(ke):
-        ths.copy_(th_h); als.copy_(al_h); bes.copy_(be_h)   # reset the init (host, untimed)
+    W = T_h.numel()
+    bi = sum(x.numel() * x.element_size() for x in (t_h, m_h, o_h, T_h, th0, al0, be0))
+    bo = (th0.numel() + al0.numel() + be0.numel()) * 4 + W * (8 + 4 + 4)
+    M.fit_host(D, t_h, m_h, o_h, T_h, ths, als, bes, cfg, time_mode=1)   # warm-up (workspace pool)
+    times = []
+    for _ in range(calls):
+        ths.copy_(th0); als.copy_(al0); bes.copy_(be0)   # reset the init (host, untimed)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         M.fit_host(D, t_h, m_h, o_h, T_h, ths, als, bes, cfg, time_mode=1)
-        dt += time.perf_counter() - t0
-    dt /= ke
+        times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times)
     dtt = torch.tensor([dt], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(dtt, op=dist.ReduceOp.MAX)
-    return {"value": ev_it_per_step / float(dtt), "unit": UNIT,
-            "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo), "steps": ke,
-            "api": "mdhp_fit_host (pinned host CSR in, fitted params/lnL/iters/status out)"}
+    return {"value": res["ev_it_per_step"] / float(dtt), "unit": UNIT,
+            "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo), "steps": calls,
+            "call_s": [round(x, 4) for x in times],
+            "api": "mdhp_fit_host (pinned host CSR share in, fitted params/lnL/iters/status out; "
+                   "per rank, max over ranks)"}
+
+
+def oracle_lnl_parity(D, d, windows, time_mode=1):
+    """lnL parity of returned results: the fp64 oracle (convert_window + loglik_batch on all host
+    cores) evaluates Eq.(5) at the parameters the GPU returned, for the listed windows of this
+    rank's batch; -> {max_rel_lnl, n_windows_checked, bar}.  Part of the cpu_baseline leg (the
+    one place bench.py runs oracle/ besides --impl reference)."""
+    import numpy as np
+    import oracle
+    t_all = d["t"].cpu().numpy(); m_all = d["mark"].cpu().numpy()
+    off_all = d["win_off"].cpu().numpy(); T_all = d["T"].cpu().numpy()
+    ts, ms, Ts = [], [], []
+    for w in windows:
+        a, z = int(off_all[w]), int(off_all[w + 1])
+        t32, T32, _ = oracle.convert_window(D, t_all[a:z], m_all[a:z], float(T_all[w]), time_mode,
+                                            tie_policy=oracle.TIE_NUDGE)
+        ts.append(t32); ms.append(m_all[a:z]); Ts.append(T32)
+    off = np.zeros(len(windows) + 1, np.int64)
+    off[1:] = np.cumsum([len(x) for x in ts])
+    idx = np.asarray(windows)
+    p = [d[k][idx].double().cpu().numpy() for k in ("theta", "alpha", "beta")]
+    t0 = time.perf_counter()
+    ref = oracle.loglik_batch(D, np.concatenate(ts), np.concatenate(ms).astype(np.int32), off, np.asarray(Ts),
+                              *p, grads=False)
+    got = d["lnl"].cpu().numpy()[idx]
+    rel = np.abs(got - ref["lnl"]) / np.abs(ref["lnl"])
+    return {"max_rel_lnl": float(rel.max()), "n_windows_checked": int(len(idx)), "bar": 1e-4,
+            "what": "GPU lnL at the returned parameters vs the fp64 oracle's Eq.(5) at the same parameters",
+            "oracle_s": round(time.perf_counter() - t0, 2)}
+
+
+def strided(W, n):
+    step = max(1, W // n)
+    return sorted(set(range(0, W, step)) | {W - 1})
 
 
 class ClockSampler:
@@ -366,31 +524,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(b_host, D, rc, iters, n_windows, seed):
-    """The fp64 oracle (as it stands: oracle_fit_batch on a pthread pool over all host cores) on
-    a bounded sample of the same workload: the first n_windows windows, `iters` iterations."""
-    import numpy as np
-    import oracle
-    W = n_windows
-    off = b_host["win_off"][: W + 1]
-    E = int(off[-1])
-    t32 = np.asarray(b_host["t"][:E], np.float64) / rc.T   # UNIT == RAW here (T = 1 s)
-    t32 = t32.astype(np.float32)
-    mark = np.asarray(b_host["mark"][:E], np.int32)
-    th = np.full((W, D), 0.1); al = np.full((W, D, D), 0.5); be = np.full((W, D, D), 1.0)
-    cfg = oracle.FitConfig(max_iters=iters, optimizer="adam", lr=0.05, tol_rel=0.0)
-    ncores = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    r = oracle.fit_batch(D, t32, mark, off, np.full(W, 1.0), th, al, be, cfg, nthreads=ncores)
-    dt = time.perf_counter() - t0
-    evals = (r["iters"].astype(np.int64) + 1)
-    ev_it = float(np.sum(np.diff(off) * evals))
-    return {"value": ev_it / dt, "unit": UNIT, "cores": ncores, "kind": "oracle",
-            "sample": f"{W} windows of the same workload x {iters} Adam iterations (+1 final evaluation), "
-                      f"fp64 eager recursion, {dt:.1f} s wall", "windows_per_s": W / dt,
-            "cpu_model": cpu_model()}
-
-
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -430,21 +563,164 @@ def reference_arm(args):
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
-    ev_it = float(np.sum(np.diff(off) * (r["iters"].astype(np.int64) + 1)))
-    tm = max(times) if times else float("nan")
+    ev_it = float(np.sum(np.diff(off) * r["iters"].astype(np.int64)))   # iterations (as our arm)
     val = ev_it / (sum(times) / len(times))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Ogata-thinned MDHP, seed %d)" % args.seed,
             "config": {"workload": f"{args.config} (sample: {nw} windows x {it} Adam iterations per step)",
                        "D": D, "windows": nw, "iterations": it},
             "windows_fitted_per_s": nw / (sum(times) / len(times)),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": ncores, "kind": "oracle",
-                             "sample": f"{nw} windows of {args.config} x {it} Adam iterations (+1 final eval) per step"},
+                             "sample": f"{nw} windows of {args.config} x {it} Adam iterations (+1 final eval) "
+                                       "per step, counted as event-iterations like our arm"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def run_seq(M, rc, iters, steps, warmup, seed, first, dev, chunk=0, parity=False):
+    """cfg4: one long sequence fitted by the chunked-scan path (a7, mdhp_seq_fit); returns the
+    measurements (+ lnL parity of the returned parameters against the oracle on the fp64 times)."""
+    import numpy as np
+    import torch
+    from synth import gpu as sgpu
+    D = rc.D
+    b = sgpu.make_batch_gpu(rc, 1, seed=seed, first_window=first, device=dev)
+    N = int(b["win_off"][-1])
+    ce = chunk or M.seq_chunk_hint(D, N)
+    ps = M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=ce)
+    th0 = b["theta"][0].clone(); al0 = b["alpha"][0].clone(); be0 = b["beta"][0].clone()
+    th, al, be = th0.clone(), al0.clone(), be0.clone()
+    cfg = M.FitConfig(max_iters=iters, optimizer="adam", lr=0.05, tol_rel=0.0)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        th.copy_(th0); al.copy_(al0); be.copy_(be0)
+        M.seq_pack(D, b["t"], b["mark"], rc.T, chunk_events=ce, out=ps)
+        return M.seq_fit(ps, th, al, be, cfg)
+    for _ in range(max(warmup, 1)):
+        r = step()
+    torch.cuda.synchronize()
+    it = int(r["iters"][0])
+    L0 = M.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        r = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    out = {"value": N * it / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "us_per_iteration": 1e3 * ms / (it + 1),
+           "events": N, "chunk_events": ce, "iterations": it, "launches_per_step": (M.launch_count() - L0) / steps,
+           "roofline": roofline_of(D, N * (it + 1), ms, "k_seq (all phases)")}
+    if parity:
+        import oracle
+        t0 = time.perf_counter()
+        ref = oracle.loglik_rec(D, b["t"].cpu().numpy(), b["mark"].cpu().numpy(), rc.T, th.double().cpu().numpy(),
+                                al.double().cpu().numpy(), be.double().cpu().numpy(), grads=False)
+        got = float(r["lnl"][0])
+        out["parity"] = {"max_rel_lnl": abs(got - ref["lnl"]) / abs(ref["lnl"]), "n_windows_checked": 1, "bar": 1e-4,
+                         "what": "GPU lnL at the returned parameters vs the fp64 oracle (fp64 times)",
+                         "oracle_s": round(time.perf_counter() - t0, 2)}
+    return out
+
+
+def bench_seq(args, rc, world, rank, dev):
+    """--config cfg4: one long sequence per GPU (replicas at N > 1: the sequence path does not
+    shard, DESIGN.md section 7), fitted by the chunked-scan path (mdhp_seq_fit)."""
+    import torch.distributed as dist
+    import paper_2411_10258_b200 as M
+    if args.shard_seq:
+        return bench_seq_sharded(args, rc, world, rank, dev)
+    o = run_seq(M, rc, args.iters, args.steps, args.warmup, args.seed, rank, dev, chunk=args.chunk)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": world * o["value"], "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": o["ms_per_step"],
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                          "data": f"synthetic (Ogata-thinned MDHP on GPU, recipe cfg4, seed {args.seed})",
+                          "config": {"workload": f"cfg4: one sequence/GPU, D={rc.D}, {o['events']} events over "
+                                                 f"{rc.T}s, chunked scan ({o['chunk_events']} events/chunk), Adam "
+                                                 f"lr 0.05, {args.iters} fixed iterations + final eval",
+                                     "events": o["events"], "us_per_iteration": o["us_per_iteration"]},
+                          "roofline": o["roofline"], "gpu_launches": int(o["launches_per_step"] * args.steps)}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def sub_results(M, args, dev):
+    """N = 1: one line per BASELINE config besides the headline, each measured the way the paper's
+    per-config numbers are quoted, with its roofline fraction and lnL parity."""
+    from synth import gen
+    subs = {}
+    plan = [("cfg1", 1, 500, 0.0, 5, 3), ("cfg2", 4096, 500, 0.0, 3, 2), ("cfg3", 65536, 500, 0.0, 1, 1)]
+    for name, W, iters, tol, steps, warm in plan:
+        rc = gen.CONFIGS[name]
+        cfg = fit_cfg_for(M, name, iters, tol)
+        r = run_windows(M, rc, name, W, cfg, 1, 0, dev, steps, warm, True, args.seed, keep=True)
+        d = r["data"]
+        sub = {"workload": f"{name}: {W} windows, D={rc.D}, ~{r['local_E'] // max(W, 1)} events/window, T={rc.T}s, "
+                           + ("plain GD lr 0.5 on the mean loss" if name == "cfg1" else "Adam lr 0.05")
+                           + f", {iters} fixed iterations + final eval",
+               "value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
+               "windows_fitted_per_s": r["windows_fitted_per_s"], "fit_ms": r["fit_ms"],
+               "roofline": roofline_of(rc.D, r["local_ev_eval"], r["fit_ms"], "k_fit")}
+        if name == "cfg1":
+            sub["latency_ms_per_window_fit"] = r["fit_ms"]
+        if not args.no_cpu:
+            sub["parity"] = oracle_lnl_parity(rc.D, d, strided(W, 4096 if name != "cfg3" else 1024))
+        subs[name] = sub
+        del r, d
+    rc = gen.CONFIGS["cfg4"]
+    o = run_seq(M, rc, 500, 3, 2, args.seed, 0, dev, parity=not args.no_cpu)
+    o["workload"] = f"cfg4: one sequence, D={rc.D}, {o['events']} events, chunked scan, Adam lr 0.05, 500 fixed iterations"
+    subs["cfg4"] = o
+    # cfg5 converged mode (SURVEY 8(d)): tol_rel 1e-6, patience 10, at most 500 iterations
+    rc = gen.CONFIGS["cfg5"]
+    cfg = fit_cfg_for(M, "cfg5", 500, 1e-6)
+    r = run_windows(M, rc, "cfg5", 1 << 20, cfg, 1, 0, dev, 1, 1, True, args.seed, keep=True)
+    sub = {"workload": "cfg5 converged mode: 1,048,576 windows, D=16, Adam lr 0.05, tol_rel 1e-6, patience 10, "
+                       f"at most 500 iterations (mean {r['mean_iters']:.1f}) + final eval",
+           "value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
+           "windows_fitted_per_s": r["windows_fitted_per_s"], "fit_ms": r["fit_ms"],
+           "roofline": roofline_of(16, r["local_ev_eval"], r["fit_ms"], "k_fit (refill)")}
+    if not args.no_cpu:
+        sub["parity"] = oracle_lnl_parity(16, r["data"], strided(1 << 20, 4096))
+    subs["cfg5_converged"] = sub
+    return subs
+
+
+def cpu_baseline(d, D, iters, n_windows):
+    """The fp64 oracle (as it stands: oracle_fit_batch on a pthread pool over all host cores) on
+    a bounded sample of the same workload: the first n_windows windows, `iters` iterations."""
+    import numpy as np
+    import oracle
+    W = n_windows
+    off = d["win_off"][: W + 1].cpu().numpy()
+    E = int(off[-1])
+    t = d["t"][:E].cpu().numpy()
+    mark = d["mark"][:E].cpu().numpy().astype(np.int32)
+    T = d["T"][:W].cpu().numpy()
+    ts = []
+    for w in range(W):
+        t32, T32, _ = oracle.convert_window(D, t[off[w]:off[w + 1]], mark[off[w]:off[w + 1]], float(T[w]), 1,
+                                            tie_policy=oracle.TIE_NUDGE)
+        ts.append(t32)
+    t32 = np.concatenate(ts)
+    th = np.full((W, D), 0.1); al = np.full((W, D, D), 0.5); be = np.full((W, D, D), 1.0)
+    cfg = oracle.FitConfig(max_iters=iters, optimizer="adam", lr=0.05, tol_rel=0.0)
+    ncores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    r = oracle.fit_batch(D, t32, mark, off, np.full(W, 1.0), th, al, be, cfg, nthreads=ncores)
+    dt = time.perf_counter() - t0
+    ev_it = float(np.sum(np.diff(off) * r["iters"].astype(np.int64)))
+    return {"value": ev_it / dt, "unit": UNIT, "cores": ncores, "kind": "oracle",
+            "sample": f"{W} windows of the same workload x {iters} Adam iterations (+1 final evaluation), "
+                      f"fp64 eager recursion, {dt:.1f} s wall", "windows_per_s": W / dt,
+            "cpu_model": cpu_model()}
 
 
 def main():
@@ -452,13 +728,11 @@ def main():
     if args.impl == "reference":
         return reference_arm(args)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2411_10258_b200 as M
     from synth import gen
-    from synth import gpu as sgpu
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -475,154 +749,92 @@ def main():
         rc = dataclasses.replace(rc, inject=args.inject)
     D = rc.D
     W = args.windows or wdef
-    stream = torch.cuda.current_stream()
-
-    # ---- synthetic inputs (untimed): windows rank*W .. rank*W+W-1 of the global seeded stream
     if args.config == "cfg4":
         return bench_seq(args, rc, world, rank, dev)
     if args.config == "feat":
         return bench_features(args, world, rank, dev)
-    first, _ = (rank * W, W)
-    b = sgpu.make_batch_gpu(rc, W, seed=args.seed, first_window=first, device=dev)
     if args.loglik:
+        from synth import gpu as sgpu
+        b = sgpu.make_batch_gpu(rc, W, seed=args.seed, first_window=rank * W, device=dev)
         return bench_loglik(args, rc, b, W, world, rank, dev)
-    E = int(b["win_off"][-1])
-    init_th = torch.full((W, D), 0.1, device=dev)
-    init_al = torch.full((W, D, D), 0.5, device=dev)
-    init_be = torch.full((W, D, D), 1.0, device=dev)
-    th, al, be = init_th.clone(), init_al.clone(), init_be.clone()
-    cfg = M.FitConfig(max_iters=args.iters, optimizer="adam", lr=0.05, tol_rel=args.tol, patience=10)
-    from paper_2411_10258_b200 import shard
-    rec = torch.empty(W, shard.record_width(D), dtype=torch.float32, device=dev)
-    gathered = [torch.empty_like(rec) for _ in range(world)] if (world > 1 and rank == 0) else None
-    packed = None
-    fit_ev0, fit_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
-    def step(timing_fit=None):
-        nonlocal packed
-        th.copy_(init_th); al.copy_(init_al); be.copy_(init_be)
-        packed = M.pack_windows(D, b["t"], b["mark"], b["win_off"], b["T"], time_mode=1, out=packed)
-        if timing_fit is not None:
-            timing_fit[0].record(stream)
-        r = M.fit(packed, th, al, be, cfg)
-        if timing_fit is not None:
-            timing_fit[1].record(stream)
-        if world > 1:   # a8: one gather of fixed-size per-window records to rank 0
-            shard.pack_records(th, al, be, r["lnl"], r["iters"], r["status"], out=rec)
-            shard.gather_records(rec, world, rank, out=gathered)
-        return r
-
-    for _ in range(max(args.warmup, 1)):   # at least one: the iteration counts come from it
-        r = step()
-    torch.cuda.synchronize()
-    iters_run = r["iters"].to(torch.int64)
-    ev_it_step = int(((b["win_off"][1:] - b["win_off"][:-1]) * (iters_run + 1)).sum())  # + final evaluation
-
+    strong = not args.weak
+    cfg = fit_cfg_for(M, args.config, args.iters, args.tol)
     clocks = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
                           int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    L0 = M.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    fit_ms = []
-    e0.record(stream)
-    for _ in range(args.steps):
-        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-        r = step(ev)
-        fit_ms.append(ev)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    launches = M.launch_count() - L0
-    ms = e0.elapsed_time(e1)
-    fit_avg = sum(a.elapsed_time(z) for a, z in fit_ms) / len(fit_ms)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_max = float(t_max)
-    total_ev_it = ev_it_step * args.steps
-    tot = torch.tensor([float(total_ev_it), float(W * args.steps)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot)
-    value = float(tot[0]) / (ms_max / 1e3)
-    wps = float(tot[1]) / (ms_max / 1e3)
+    res = run_windows(M, rc, args.config, W, cfg, world, rank, dev, args.steps, args.warmup, strong,
+                      args.seed, clocks=clocks, keep=True)
+    d = res["data"]
+    value = res["value"]
 
     # ---- end to end through the public C ABI on HOST buffers (mdhp_fit_host), copies inside
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(M, b, D, W, cfg, init_th, init_al, init_be, float(tot[0]) / args.steps, world, dev)
+        e2e = run_e2e(M, res, D, cfg, world, dev)
 
     # ---- roofline of the dominant kernel (k_fit): algorithmic MUFU ops / its CUDA-event time
-    mufu_per_ev = 2 * D + 2
-    achieved = ev_it_step * mufu_per_ev / (fit_avg / 1e3) / 1e9
-    # DRAM traffic of this launch from the committed ncu capture of the same launch config
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "r01_k_fit_traffic_cfg5.json")
-    if os.path.exists(tf):
-        tj = json.load(open(tf))
-        if tj["windows"] == W and tj["events"] == E and tj["evaluations_per_window"] == args.iters + 1:
-            traffic = tj["traffic_bytes_per_launch"]
-    # shared-memory roofline of the same kernel: algorithmic smem bytes per event-evaluation
-    # (row {alpha,beta}+{S,Q'} 16 B, column beta+{S,Q'} 12 B + {S,Q'} store 8 B, gradient RMW 16 B,
-    # per lane, Dp lanes) against 128 B/clk/SM
+    roof = roofline_of(D, res["local_ev_eval"], res["fit_ms"], "k_fit")
     Dp = 1 << (D - 1).bit_length()
-    smem_bytes = ev_it_step * 52 * Dp
-    smem_peak = 148 * 128 * 1.965   # GB/s at clocks.max.sm
+    cap = kernel_capture(res["local_W"], res["local_E"], args.iters + 1) if args.tol <= 0 else None
+    roof["traffic"] = cap["dram_bytes"] if cap else None
+    roof["traffic_source"] = (f"{os.path.relpath(CAPTURE, ROOT)} (ncu, source hash {cap['source_hash']})"
+                              if cap else "no ncu capture of this kernel source and launch")
     # the binding pipe of this design: shared-memory wavefronts and warp
-    # shuffles share one MIO slot per clock per SM (profiles/r01_ubench_b200.txt).  Per
-    # event-evaluation: 52*Dp/128 wavefronts + the reduction/broadcast slots per window-event
-    # (per 8-event chunk and warp: reduce-scatter + theta shuffle + weight broadcast, / G*8)
+    # shuffles share one MIO slot per clock per SM (profiles/r01_ubench_b200.txt).  Algorithmic
+    # count per event-evaluation: 52*Dp/128 wavefronts + the reduction/broadcast slots
     shfl_per_ev = {8: 11 / 32, 16: 12 / 16, 32: 18 / 8}.get(Dp, 0.0)
     mio_per_ev = 52 * Dp / 128 + shfl_per_ev
-    mio_peak = 148 * 1.965   # G slots/s
-    mio_ach = ev_it_step * mio_per_ev / (fit_avg / 1e3) / 1e9
-    mio = {"achieved_Gslots": mio_ach, "peak_Gslots": mio_peak, "frac": mio_ach / mio_peak,
-           "per_unit": f"{mio_per_ev:.3f} MIO slots per event-iteration (shared wavefronts + shuffles)"}
-    if Dp == 16:
-        # the same pipe measured by ncu on this kernel (all shared wavefronts incl. the
-        # non-loop phases, plus SHFL), not the algorithmic count above
-        mio["ncu_measured_frac"] = 0.848
-        mio["ncu_source"] = ("profiles/r01_k_fit_fullsize_mio.txt (this launch configuration: shared "
-                             "wavefronts 79.1% + SHFL 5.7% of all SM cycles)")
-    roof = {"bound": "alu", "achieved": achieved, "peak": MUFU_PEAK_GOPS, "unit": "Gop/s (MUFU)",
-            "frac": achieved / MUFU_PEAK_GOPS, "traffic": traffic, "kernel": f"k_fit<{Dp}>",
-            "per_unit": f"{mufu_per_ev} MUFU ops per event-iteration (2D ex2 + lg2 + rcp)",
-            "peak_basis": "148 SMs x 16 MUFU/clk x 1.965 GHz (guide unit count x clocks.max.sm); "
-                          "measured ex2 rate 4618 Gop/s (profiles/r01_ubench_b200.txt)",
-            "smem": {"achieved_GBps": smem_bytes / (fit_avg / 1e3) / 1e9, "peak_GBps": smem_peak,
-                     "frac": smem_bytes / (fit_avg / 1e3) / 1e9 / smem_peak,
-                     "per_unit": f"{52 * Dp} B shared-memory traffic per event-iteration"},
-            "mio": mio,
-            "fit_ms_avg": fit_avg, "fit_share_of_step": fit_avg / (ms / args.steps)}
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        nw = args.cpu_windows or 8192
-        bh = {"t": b["t"][: int(b["win_off"][nw])].cpu().numpy(), "mark": b["mark"][: int(b["win_off"][nw])].cpu().numpy(),
-              "win_off": b["win_off"][: nw + 1].cpu().numpy()}
-        cpu = cpu_baseline(bh, D, rc, 5, nw, args.seed)
+    mio_ach = res["local_ev_eval"] * mio_per_ev / (res["fit_ms"] / 1e3) / 1e9
+    roof["mio"] = {"achieved_Gslots": mio_ach, "peak_Gslots": MIO_PEAK_GSLOTS, "frac": mio_ach / MIO_PEAK_GSLOTS,
+                   "per_unit": f"{mio_per_ev:.3f} MIO slots per event-evaluation (shared wavefronts + shuffles, "
+                               "algorithmic count)"}
+    if cap and "mio_frac" in cap:
+        roof["mio"]["ncu_measured_frac"] = cap["mio_frac"]
+    roof["fit_ms_avg"] = res["fit_ms"]
+    roof["fit_share_of_step"] = res["fit_ms"] / res["ms_per_step"]
+
+    cpu = parity = None
+    subs = None
+    if rank == 0 and not args.no_cpu:
+        parity = oracle_lnl_parity(D, d, strided(res["local_W"], 65536 if args.config == "cfg5" else 4096))
+        if world == 1:
+            cpu = cpu_baseline(d, D, 5, min(args.cpu_windows or 8192, res["local_W"]))
+    del d, res["data"]
+    torch.cuda.empty_cache()
+    if world == 1 and not args.no_sub and args.config == "cfg5" and args.tol <= 0:
+        subs = sub_results(M, args, dev)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
             "data": f"synthetic (Ogata-thinned MDHP on GPU, recipe {rname}, seed {args.seed}"
                     + (f", {args.inject} injections in attack windows" if args.inject != "none" else "") + ")",
-            "config": {"workload": f"{args.config}: {W} windows/GPU, D={D}, ~{E // max(W, 1)} events/window, "
-                                   f"T={rc.T}s, Adam lr 0.05, "
+            "config": {"workload": f"{args.config}: one batch of {W} windows" + (" per GPU" if not strong else
+                                   f" split over {world} GPU(s) by equal event totals")
+                                   + f", D={D}, ~{res['local_E'] // max(res['local_W'], 1)} events/window, T={rc.T}s, "
+                                   + ("plain GD lr 0.5 (mean loss)" if args.config == "cfg1" else "Adam lr 0.05") + ", "
                                    + (f"{args.iters} fixed iterations + final eval" if args.tol <= 0 else
                                       f"converged mode: tol_rel {args.tol:g}, patience 10, at most {args.iters} "
-                                      f"iterations (mean {float(iters_run.double().mean()):.1f}) + final eval"),
-                       "windows_per_gpu": W, "events_per_gpu": E, "D": D, "iterations": args.iters,
-                       "l2": "inputs larger than L2 (packed events ~%.1f GB/GPU vs 126 MB L2)" % (E * 9 / 1e9),
-                       "parallelism": f"windows sharded over {world} GPU(s), final NCCL gather"},
-            "windows_fitted_per_s": wps,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk,
+                                      f"iterations (mean {res['mean_iters']:.1f}) + final eval"),
+                       "windows": W, "D": D, "iterations": args.iters,
+                       "event_iterations_per_step": res["ev_it_per_step"],
+                       "event_evaluations_per_step": res["ev_eval_per_step"],
+                       "value_counts": "event-iterations (optimizer steps); the final lnL evaluation is "
+                                       "in event_evaluations_per_step, not in value",
+                       "l2": "inputs larger than L2 (packed events ~%.1f GB/GPU vs 126 MB L2)"
+                             % (res["local_E"] * 9 / 1e9),
+                       "parallelism": (f"one batch split over {world} GPU(s) (balanced_ranges), final NCCL "
+                                       "gather + reassembly on rank 0" if strong else
+                                       f"weak: {W} windows per GPU, final NCCL gather"),
+                       "per_rank": res["per_rank"], "imbalance_fit_max_over_mean": res["imbalance"],
+                       "fit_ms_max_over_ranks": res["fit_ms_max_over_ranks"]},
+            "windows_fitted_per_s": res["windows_fitted_per_s"],
+            "roofline": roof, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(res["launches"]), "clocks": res["clocks"],
         }
+        if subs:
+            line["configs"] = subs
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -121,3 +121,88 @@ def test_slice_bounds_never_split_ties():
         assert b[0][0] == 0 and b[-1][1] == len(t) and all(b[k][1] == b[k + 1][0] for k in range(R - 1))
         for lo, hi in b:
             assert lo == 0 or lo == len(t) or t[lo] != t[lo - 1]
+
+
+def _fake_fit(t, mark, win_off, T, D):
+    """A deterministic per-window stand-in for pack + fit (CPU): results depend only on the
+    window's own events, so any split of the batch must reassemble to the unsplit results."""
+    W = len(T)
+    th = torch.zeros(W, D); al = torch.zeros(W, D, D); be = torch.zeros(W, D, D)
+    lnl = torch.zeros(W, dtype=torch.float64)
+    for w in range(W):
+        a, z = int(win_off[w]), int(win_off[w + 1])
+        cnt = torch.bincount(mark[a:z].long(), minlength=D).float()
+        th[w] = cnt / float(T[w])
+        al[w] = torch.outer(cnt, cnt) / (1.0 + (z - a) % 7)
+        be[w] = float(t[a:z].sum()) + torch.arange(D * D, dtype=torch.float32).view(D, D)
+        lnl[w] = float(t[a:z].double().sum()) - 1e-3 * (z - a)
+    it = (win_off[1:] - win_off[:-1]).to(torch.int32)
+    st = torch.where(it == 0, 1, 0).to(torch.int32)
+    return th, al, be, lnl, it, st
+
+
+def _strong_batch(W=53, D=4, seed=3):
+    g = torch.Generator().manual_seed(seed)
+    n = torch.randint(0, 30, (W,), generator=g)
+    off = torch.zeros(W + 1, dtype=torch.int64)
+    off[1:] = torch.cumsum(n, 0)
+    E = int(off[-1])
+    t = torch.rand(E, generator=g, dtype=torch.float64)
+    mark = torch.randint(0, D, (E,), generator=g, dtype=torch.int32)
+    T = torch.ones(W, dtype=torch.float64)
+    return t, mark, off, T
+
+
+def _strong_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    D = 4
+    t, mark, off, T = _strong_batch(D=D)
+    ranges = shard.balanced_ranges((off[1:] - off[:-1]).numpy(), world)
+    lo, hi = ranges[rank]
+    res = _fake_fit(*shard.slice_csr(t, mark, off, T, lo, hi), D)
+    n_max = max(z - a for a, z in ranges)
+    rec = torch.zeros(n_max, shard.record_width(D))
+    out = shard.gather_step(*res, rec, ranges, world, rank)
+    if rank == 0:
+        ref = _fake_fit(t, mark, off, T, D)
+        ok = all(torch.equal(out[k], v) for k, v in zip(("theta", "alpha", "beta", "lnl", "iters", "status"), ref))
+        q.put(("ok" if ok else "mismatch", ranges))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_strong_step_world2_gloo():
+    """The strong-scaling step logic of bench.py on CPU, world size 2: balanced ranges of ONE
+    batch -> CSR slices -> per-rank (stand-in) fits -> padded records -> gather -> reassembly in
+    global window order on rank 0 == the unsplit batch's results bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_strong_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+        assert p.exitcode == 0
+    status, ranges = q.get(timeout=5)
+    assert status == "ok" and ranges[0][0] == 0 and ranges[-1][1] == 53 and ranges[0][1] == ranges[1][0]
+
+
+def test_slice_csr_and_reassemble_single_process():
+    D = 3
+    t, mark, off, T = _strong_batch(W=40, D=D, seed=9)
+    ref = _fake_fit(t, mark, off, T, D)
+    for world in (1, 3, 5, 8):
+        ranges = shard.balanced_ranges((off[1:] - off[:-1]).numpy(), world)
+        n_max = max(z - a for a, z in ranges)
+        recs = []
+        for r, (lo, hi) in enumerate(ranges):
+            res = _fake_fit(*shard.slice_csr(t, mark, off, T, lo, hi), D)
+            rec = torch.zeros(n_max, shard.record_width(D))
+            shard.pack_records(*res, out=rec[: hi - lo])
+            recs.append(rec)
+        out = shard.reassemble(recs, ranges, D)
+        for k, v in zip(("theta", "alpha", "beta", "lnl", "iters", "status"), ref):
+            assert torch.equal(out[k], v), (world, k)
