@@ -141,6 +141,85 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- TMEM as per-lane storage
+// tcgen05.ld/st with the 32x32b shape move 32-bit columns between thread l of a warp and TMEM
+// lane 32*(warp%4)+l: a per-lane array indexed by a warp-uniform column.  The fit kernel keeps
+// each window's optimizer state there (k_fit, DESIGN.md a6).  All lanes of a warp must execute
+// these (.sync.aligned); values loaded by tm_ld are valid only after tm_wait_ld on them.
+template <int N>
+__device__ __forceinline__ void tm_ld(uint32_t a, float (&v)[N]) {
+  static_assert(N == 1 || N == 2 || N == 4 || N % 8 == 0, "tm_ld width");
+  if constexpr (N == 1) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=f"(v[0]) : "r"(a));
+  } else if constexpr (N == 2) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                 : "=f"(v[0]), "=f"(v[1]) : "r"(a));
+  } else if constexpr (N == 4) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(a));
+  } else {
+#pragma unroll
+    for (int k = 0; k < N; k += 8)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                   : "=f"(v[k]), "=f"(v[k + 1]), "=f"(v[k + 2]), "=f"(v[k + 3]), "=f"(v[k + 4]),
+                     "=f"(v[k + 5]), "=f"(v[k + 6]), "=f"(v[k + 7])
+                   : "r"(a + (uint32_t)k));
+  }
+}
+template <int N>
+__device__ __forceinline__ void tm_st(uint32_t a, const float (&v)[N]) {
+  static_assert(N == 1 || N == 2 || N == 4 || N % 8 == 0, "tm_st width");
+  if constexpr (N == 1) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(a), "f"(v[0]) : "memory");
+  } else if constexpr (N == 2) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(a), "f"(v[0]),
+                 "f"(v[1]) : "memory");
+  } else if constexpr (N == 4) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                 "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]) : "memory");
+  } else {
+#pragma unroll
+    for (int k = 0; k < N; k += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+                   ::"r"(a + (uint32_t)k), "f"(v[k]), "f"(v[k + 1]), "f"(v[k + 2]), "f"(v[k + 3]),
+                   "f"(v[k + 4]), "f"(v[k + 5]), "f"(v[k + 6]), "f"(v[k + 7]) : "memory");
+  }
+}
+// Wait for the outstanding tcgen05.ld of this thread; the registers pass through the asm so no
+// use of them can be scheduled before the wait.
+__device__ __forceinline__ void tm_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void tm_fence_regs(float (&v)[N]) {
+#pragma unroll
+  for (int k = 0; k < N; k++) asm volatile("" : "+f"(v[k]));
+}
+__device__ __forceinline__ void tm_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// Allocate `cols` (a power of two >= 32) TMEM columns for the CTA (warp 0), publish the base
+// through shared memory and synchronise the CTA; returns the base address.
+__device__ __forceinline__ uint32_t tm_alloc(uint32_t* slot, uint32_t cols) {
+  if ((threadIdx.x >> 5) == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(slot))),
+                 "r"(cols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  return *reinterpret_cast<volatile uint32_t*>(slot);
+}
+__device__ __forceinline__ void tm_free(uint32_t base, uint32_t cols) {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols)
+                 : "memory");
+}
+
 template <int DP>
 __device__ __forceinline__ float group_sum(float v) {
 #pragma unroll

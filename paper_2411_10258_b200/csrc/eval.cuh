@@ -245,8 +245,10 @@ __device__ __forceinline__ void sts2o(uint32_t a, float x, float y) {
 }
 
 // One chunk of 8 events (see event_loop).  A, SQ, Gs are one group's arrays laid out
-// contiguously (SQ = A + AS, Gs = A + 2 AS; Smem<DP>).
-template <int DP, bool GRAD>
+// contiguously (SQ = A + AS, Gs = A + 2 AS; Smem<DP>).  PRE: A holds beta' = -beta log2(e)
+// (the fit and loglik kernels) instead of beta (the sequence path), so every exponential is
+// ex2(beta' * dt) without the extra multiply.
+template <int DP, bool GRAD, bool PRE>
 __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __restrict__ A,
                                               float2* __restrict__ SQ, float2* __restrict__ Gs,
                                               const int j, const int gbase, const float th,
@@ -283,8 +285,8 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     const float2 sc = lds2o<kSQ>(ca);
     const float dr = t - last;
     const float a_ij = ab_alpha<DP>(i, ar), b_ij = ab_beta<DP>(i, ar);
-    const float er = ex2f(b_ij * (dr * -kLog2e));
-    const float ec = ex2f(bc * (dc * -kLog2e));
+    const float er = PRE ? ex2f(b_ij * dr) : ex2f(b_ij * (dr * -kLog2e));
+    const float ec = PRE ? ex2f(bc * dc) : ex2f(bc * (dc * -kLog2e));
     const float R = fmaf(er, sr.x, -fset_eq0(dr));   // strict T_j^k < t
     // theta_i enters after the reduction for DP >= 8 (below), through lane i for DP <= 4
     const float p = DP >= 8 ? a_ij * R : fmaf(a_ij, R, fsel_eqi(i, j, th, 0.0f));
@@ -308,8 +310,14 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
       }
       lacc += (j == 0) ? lg2f(lam) : 0.0f;
     }
+    // no __syncwarp per event (it cost an issue slot each): the state accesses are volatile asm
+    // in program order and the warp is converged, so the shared-memory unit sees one event's
+    // column stores before the next event's row loads
+#ifdef MDHP_AB_EVENT_SYNCWARP
     __syncwarp();
+#endif
   }
+  __syncwarp();
   if constexpr (DP >= 8) {
     // this lane now holds event e's sum over sources; add theta of its mark (0 for a null
     // event), which lane gbase + mark holds
@@ -357,7 +365,7 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
 
 // The event loop of one window-evaluation, two chunks per iteration with explicit buffers so
 // the prefetch of chunk c+1 overlaps chunk c without register rotation.
-template <int DP, bool GRAD>
+template <int DP, bool GRAD, bool PRE>
 __device__ __forceinline__ void event_loop(const float2* __restrict__ A, float2* __restrict__ SQ,
                                            float2* __restrict__ Gs,
                                            const int j, const int gbase,
@@ -382,11 +390,11 @@ __device__ __forceinline__ void event_loop(const float2* __restrict__ A, float2*
   load_chunk(c0, tw, dw, mw, 0 < n ? 0 : npad);
   for (int base = 0; base < nmax; base += 16) {
     load_chunk(c1, tw, dw, mw, min(base + 8, npad));
-    process_chunk<DP, GRAD>(c0, A, SQ, Gs, j, gbase, th, last, gth, lsum);
+    process_chunk<DP, GRAD, PRE>(c0, A, SQ, Gs, j, gbase, th, last, gth, lsum);
     // no early exit: a second chunk past nmax is all null events (exact no-ops), and one basic
     // block per iteration lets ptxas overlap chunk c's reduction with chunk c+1's row reads
     load_chunk(c0, tw, dw, mw, min(base + 16, npad));
-    process_chunk<DP, GRAD>(c1, A, SQ, Gs, j, gbase, th, last, gth, lsum);
+    process_chunk<DP, GRAD, PRE>(c1, A, SQ, Gs, j, gbase, th, last, gth, lsum);
   }
 }
 

@@ -1,5 +1,7 @@
 // fit.cu — mdhp_loglik_grad and mdhp_fit kernels (rows a2-a6 of DESIGN.md section 4).
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include "eval.cuh"
 
 namespace mdhp {
@@ -51,7 +53,7 @@ __device__ __forceinline__ double eval_window(const Packed& P, float2* A, float2
   const int64_t beg = live ? P.begin[w] : 0;
   float last, gth;
   double lsum;
-  event_loop<DP, GRAD>(A, SQ, Gs, c.j, c.gbase, P.t32, P.dtp, P.mark, beg, n, nmax, th, last, gth,
+  event_loop<DP, GRAD, true>(A, SQ, Gs, c.j, c.gbase, P.t32, P.dtp, P.mark, beg, n, nmax, th, last, gth,
                        lsum);
   ColInfo cc = ci;
   cc.last = last;
@@ -64,7 +66,8 @@ __device__ __forceinline__ double eval_window(const Packed& P, float2* A, float2
     const float2 k = A[i * (DP + 1) + c.j];
     const float2 sq = SQ[i * (DP + 1) + c.j];
     float Eb, Hb2;
-    const float ka = ab_alpha<DP>(i, k), kb = ab_beta<DP>(i, k);
+    // A holds beta' = -beta log2 e; the compensator takes beta (one rounding of beta' * -ln 2)
+    const float ka = ab_alpha<DP>(i, k), kb = ab_beta<DP>(i, k) * -kLn2;
     compensator(cc, S, kb, sq.x, sq.y, Eb, Hb2);
     if (cc.real && i < P.D) {
       part3 += (double)(ka * Eb);
@@ -100,7 +103,8 @@ __device__ __forceinline__ ColInfo col_info(const Packed& P, int64_t w, bool liv
   return ci;
 }
 
-// Load window parameters into K (alpha, beta) and return theta_j (0 for padded lanes).
+// Load window parameters into A = {alpha, beta' = -beta log2 e} and return theta_j (0 for
+// padded lanes).
 template <int DP>
 __device__ __forceinline__ float load_params(float2* A, const WarpCtx<DP>& c, int D, int64_t w,
                                              bool live, const float* __restrict__ theta,
@@ -114,7 +118,7 @@ __device__ __forceinline__ float load_params(float2* A, const WarpCtx<DP>& c, in
       a = alpha[(size_t)w * D * D + (size_t)i * D + c.j];
       b = beta[(size_t)w * D * D + (size_t)i * D + c.j];
     }
-    A[i * (DP + 1) + c.j] = ab_pack<DP>(i, a, b);
+    A[i * (DP + 1) + c.j] = ab_pack<DP>(i, a, b * -kLog2e);
   }
   // null dimension (see eval.cuh): row DP = {1,0} at column 0, column DP has beta = 0
   A[DP * (DP + 1) + c.j] = ab_pack<DP>(DP, c.j == 0 ? 1.0f : 0.0f, 0.0f);
@@ -166,34 +170,176 @@ k_loglik(Packed P, const float* __restrict__ theta, const float* __restrict__ al
   }
 }
 
-// One optimizer step for this lane's column j (theta_j, alpha_.j, beta_.j), PyTorch Adam / GD
-// semantics, then projection.  Gradients of lnL are in Gs (alpha, beta) and
-// dth; the loss gradient is -grad * scale.
-template <int DP, bool RESUME>
-__device__ __forceinline__ void step_column(float2* A, const float2* Gs, const WarpCtx<DP>& c,
-                                            int D, int64_t w, const FitCfgDev& cfg, float lr_w,
-                                            int s, float scale, float dth, float& th,
-                                            float* __restrict__ opt) {
-  if (c.j >= D) return;
+// ---------------------------------------------------------------- optimizer state in TMEM
+// Per window and lane j (source column j / target row j of the window's group), the state of
+// the fit that is not needed by the event loop lives in tensor memory for the whole fit and
+// touches global memory once at the start and once at the end (DESIGN.md a6): the exact beta
+// of column j (shared memory holds beta' = -beta log2 e for the event loop), the previous point
+// (rollback) and the Adam moments.  Columns (per lane, DP = padded D):
+template <int DP>
+struct TmCols {
+  static constexpr uint32_t BETA = 0, PA = DP, PB = 2 * DP, MA = 3 * DP, MB = 4 * DP,
+                            VA = 5 * DP, VB = 6 * DP, PT = 7 * DP, MT = 7 * DP + 1,
+                            VT = 7 * DP + 2, N = 7 * DP + 3;
+  static constexpr uint32_t ALLOC = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
+  static constexpr int CH = DP < 8 ? DP : 8;   // columns per tcgen05.ld/st batch
+};
+
+enum { ACT_NONE = 0, ACT_STEP = 1, ACT_ROLLBACK = 2 };
+
+// Load window w's parameters (init) into A = {alpha, beta'} (shared) and its exact beta and
+// Adam moments (opt_state or zeros) into TMEM; returns theta_j.  Warp-collective: lanes with
+// load == false keep their TMEM columns (read and written back) and their A rows.
+template <int DP>
+__device__ __forceinline__ float load_window(float2* A, const WarpCtx<DP>& c, int D, int64_t w,
+                                             bool load, bool live, uint32_t tm, float th_keep,
+                                             const float* __restrict__ theta,
+                                             const float* __restrict__ alpha,
+                                             const float* __restrict__ beta,
+                                             const float* __restrict__ opt) {
+  using L = TmCols<DP>;
+  constexpr int CH = L::CH;
+  const bool real = load && live && c.j < D;
   const size_t P = (size_t)D + 2 * (size_t)D * D;
-  float* m = opt ? opt + (size_t)w * 2 * P : nullptr;
+  const float* m = (opt && real) ? opt + (size_t)w * 2 * P : nullptr;
+  const float* v = m ? m + P : nullptr;
+#pragma unroll
+  for (int k = 0; k < DP; k += CH) {
+    float bx[CH], ma[CH], mb[CH], va[CH], vb[CH];
+    tm_ld<CH>(tm + L::BETA + k, bx);
+    tm_ld<CH>(tm + L::MA + k, ma);
+    tm_ld<CH>(tm + L::MB + k, mb);
+    tm_ld<CH>(tm + L::VA + k, va);
+    tm_ld<CH>(tm + L::VB + k, vb);
+    tm_wait_ld();
+    tm_fence_regs(bx); tm_fence_regs(ma); tm_fence_regs(mb); tm_fence_regs(va); tm_fence_regs(vb);
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+      const int i = k + u;
+      if (load) {
+        float a = 0.0f, b = 1.0f;
+        const bool r = real && i < D;
+        if (r) {
+          a = alpha[(size_t)w * D * D + (size_t)i * D + c.j];
+          b = beta[(size_t)w * D * D + (size_t)i * D + c.j];
+        }
+        A[i * (DP + 1) + c.j] = ab_pack<DP>(i, a, b * -kLog2e);
+        bx[u] = b;
+        const size_t qa = (size_t)D + (size_t)i * D + c.j, qb = qa + (size_t)D * D;
+        ma[u] = (m && r) ? m[qa] : 0.0f;
+        mb[u] = (m && r) ? m[qb] : 0.0f;
+        va[u] = (v && r) ? v[qa] : 0.0f;
+        vb[u] = (v && r) ? v[qb] : 0.0f;
+      }
+    }
+    tm_st<CH>(tm + L::BETA + k, bx);
+    tm_st<CH>(tm + L::MA + k, ma);
+    tm_st<CH>(tm + L::MB + k, mb);
+    tm_st<CH>(tm + L::VA + k, va);
+    tm_st<CH>(tm + L::VB + k, vb);
+  }
+  float mt[1], vt[1];
+  tm_ld<1>(tm + L::MT, mt);
+  tm_ld<1>(tm + L::VT, vt);
+  tm_wait_ld();
+  tm_fence_regs(mt); tm_fence_regs(vt);
+  float th = th_keep;
+  if (load) {
+    mt[0] = m ? m[c.j] : 0.0f;
+    vt[0] = v ? v[c.j] : 0.0f;
+    th = real ? theta[(size_t)w * D + c.j] : 0.0f;
+    // null dimension (see eval.cuh): row DP = {1,0} at column 0, column DP has beta = 0
+    A[DP * (DP + 1) + c.j] = ab_pack<DP>(DP, c.j == 0 ? 1.0f : 0.0f, 0.0f);
+    A[c.j * (DP + 1) + DP] = make_float2(0.0f, 0.0f);
+  }
+  tm_st<1>(tm + L::MT, mt);
+  tm_st<1>(tm + L::VT, vt);
+  tm_wait_st();
+  return th;
+}
+
+// Write window w's parameters (alpha from A, exact beta from TMEM, theta) and, when the caller
+// passed opt_state, its Adam moments back to global memory.  Warp-collective (TMEM reads);
+// only lanes with `store` write.
+template <int DP>
+__device__ __forceinline__ void store_window(const float2* A, const WarpCtx<DP>& c, int D,
+                                             int64_t w, bool store, float th, uint32_t tm,
+                                             float* __restrict__ theta, float* __restrict__ alpha,
+                                             float* __restrict__ beta, float* __restrict__ opt) {
+  using L = TmCols<DP>;
+  constexpr int CH = L::CH;
+  const bool real = store && c.j < D;
+  const size_t P = (size_t)D + 2 * (size_t)D * D;
+  float* m = (opt && real) ? opt + (size_t)w * 2 * P : nullptr;
   float* v = m ? m + P : nullptr;
+#pragma unroll
+  for (int k = 0; k < DP; k += CH) {
+    float bx[CH], ma[CH], mb[CH], va[CH], vb[CH];
+    tm_ld<CH>(tm + L::BETA + k, bx);
+    tm_ld<CH>(tm + L::MA + k, ma);
+    tm_ld<CH>(tm + L::MB + k, mb);
+    tm_ld<CH>(tm + L::VA + k, va);
+    tm_ld<CH>(tm + L::VB + k, vb);
+    tm_wait_ld();
+    tm_fence_regs(bx); tm_fence_regs(ma); tm_fence_regs(mb); tm_fence_regs(va); tm_fence_regs(vb);
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+      const int i = k + u;
+      if (real && i < D) {
+        const size_t q = (size_t)w * D * D + (size_t)i * D + c.j;
+        alpha[q] = ab_alpha<DP>(i, A[i * (DP + 1) + c.j]);
+        beta[q] = bx[u];
+        if (m) {
+          const size_t qa = (size_t)D + (size_t)i * D + c.j, qb = qa + (size_t)D * D;
+          m[qa] = ma[u]; m[qb] = mb[u]; v[qa] = va[u]; v[qb] = vb[u];
+        }
+      }
+    }
+  }
+  float mt[1], vt[1];
+  tm_ld<1>(tm + L::MT, mt);
+  tm_ld<1>(tm + L::VT, vt);
+  tm_wait_ld();
+  tm_fence_regs(mt); tm_fence_regs(vt);
+  if (real) {
+    theta[(size_t)w * D + c.j] = th;
+    if (m) {
+      m[c.j] = mt[0];
+      v[c.j] = vt[0];
+    }
+  }
+}
+
+// One optimizer action per group, warp-collective (oracle_fit):
+//   ACT_STEP      previous point <- current; PyTorch Adam / GD step on the loss -lnL * scale
+//                 for the groups in fit_mask; projection (alpha >= 0; beta, theta >= floor)
+//   ACT_ROLLBACK  current <- previous point (non-finite evaluation)
+//   ACT_NONE      nothing (the lane's TMEM columns are written back unchanged)
+// Gradients of lnL are in Gs (d alpha, d beta) and dth.  A holds {alpha, beta'}.
+template <int DP, bool RESUME>
+__device__ __forceinline__ void opt_action(float2* A, const float2* Gs, const WarpCtx<DP>& c,
+                                           int D, const FitCfgDev& cfg, int act, float lr_w,
+                                           int s, float scale, float dth, float& th, uint32_t tm) {
+#ifdef MDHP_AB_NO_OPT
+  return;   // A/B timing probe only: no optimizer action
+#endif
+  using L = TmCols<DP>;
+  constexpr int CH = L::CH;
+  const bool real = c.j < D;
+  const bool step = act == ACT_STEP, rb = act == ACT_ROLLBACK;
   const bool adam = cfg.optimizer == MDHP_OPT_ADAM;
   float bc1 = 1.0f, sbc2 = 1.0f;
-  if (adam) {
-    // s counts this call's steps; cfg.step0 those of earlier calls (resume).  A separate
-    // instantiation: reading step0 in the hot kernel perturbed its register allocation (-3%)
+  if (adam && step) {
+    // s counts this call's steps; cfg.step0 those of earlier calls (resume)
     const float sg = RESUME ? (float)(s + cfg.step0) : (float)s;
     bc1 = 1.0f - powf(cfg.b1, sg);
     sbc2 = sqrtf(1.0f - powf(cfg.b2, sg));
   }
-  auto upd = [&](float p, float g, size_t q, float lo) -> float {
+  auto upd = [&](float p, float g, float& mm, float& vv, float lo) -> float {
     const float gl = -g * scale;
     if (adam) {
-      const float mm = cfg.b1 * m[q] + (1.0f - cfg.b1) * gl;
-      const float vv = cfg.b2 * v[q] + (1.0f - cfg.b2) * gl * gl;
-      m[q] = mm;
-      v[q] = vv;
+      mm = cfg.b1 * mm + (1.0f - cfg.b1) * gl;
+      vv = cfg.b2 * vv + (1.0f - cfg.b2) * gl * gl;
       const float denom = sqrtf(vv) / sbc2 + cfg.eps;
       p = p - (lr_w / bc1) * (mm / denom);
     } else {
@@ -201,34 +347,135 @@ __device__ __forceinline__ void step_column(float2* A, const float2* Gs, const W
     }
     return p < lo ? lo : p;
   };
-  if (cfg.fit_mask & MDHP_FIT_THETA) th = upd(th, dth, (size_t)c.j, cfg.min_param);
-  for (int i = 0; i < D; i++) {
-    float2* k = &A[i * (DP + 1) + c.j];
-    const float2 gg = Gs[i * DP + c.j];
-    const size_t q = (size_t)D + (size_t)i * D + c.j;
-    float ka = ab_alpha<DP>(i, *k), kb = ab_beta<DP>(i, *k);
-    if (cfg.fit_mask & MDHP_FIT_ALPHA) ka = upd(ka, gg.x, q, 0.0f);
-    if (cfg.fit_mask & MDHP_FIT_BETA) kb = upd(kb, gg.y, q + (size_t)D * D, cfg.min_param);
-    *k = ab_pack<DP>(i, ka, kb);
+  const bool fa = cfg.fit_mask & MDHP_FIT_ALPHA, fb = cfg.fit_mask & MDHP_FIT_BETA,
+             ft = cfg.fit_mask & MDHP_FIT_THETA;
+  // alpha column (previous point, moments), then beta (exact value, previous point, moments):
+  // two passes keep fewer registers live outside the event loop
+#pragma unroll
+  for (int k = 0; k < DP; k += CH) {
+    float pa[CH], ma[CH], va[CH];
+    tm_ld<CH>(tm + L::PA + k, pa);
+    tm_ld<CH>(tm + L::MA + k, ma);
+    tm_ld<CH>(tm + L::VA + k, va);
+    tm_wait_ld();
+    tm_fence_regs(pa); tm_fence_regs(ma); tm_fence_regs(va);
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+      const int i = k + u;
+      if (real && i < D && act != ACT_NONE) {
+        float2* e = &A[i * (DP + 1) + c.j];
+        float a = ab_alpha<DP>(i, *e);
+        if (step) {
+          pa[u] = a;
+          if (fa) a = upd(a, Gs[i * DP + c.j].x, ma[u], va[u], 0.0f);
+        } else {
+          a = pa[u];
+        }
+        *e = ab_pack<DP>(i, a, ab_beta<DP>(i, *e));
+      }
+    }
+    tm_st<CH>(tm + L::PA + k, pa);
+    tm_st<CH>(tm + L::MA + k, ma);
+    tm_st<CH>(tm + L::VA + k, va);
   }
+#pragma unroll
+  for (int k = 0; k < DP; k += CH) {
+    float bx[CH], pb[CH], mb[CH], vb[CH];
+    tm_ld<CH>(tm + L::BETA + k, bx);
+    tm_ld<CH>(tm + L::PB + k, pb);
+    tm_ld<CH>(tm + L::MB + k, mb);
+    tm_ld<CH>(tm + L::VB + k, vb);
+    tm_wait_ld();
+    tm_fence_regs(bx); tm_fence_regs(pb); tm_fence_regs(mb); tm_fence_regs(vb);
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+      const int i = k + u;
+      if (real && i < D && act != ACT_NONE) {
+        float b = bx[u];
+        if (step) {
+          pb[u] = b;
+          if (fb) b = upd(b, Gs[i * DP + c.j].y, mb[u], vb[u], cfg.min_param);
+        } else {
+          b = pb[u];
+        }
+        bx[u] = b;
+        float2* e = &A[i * (DP + 1) + c.j];
+        *e = ab_pack<DP>(i, ab_alpha<DP>(i, *e), b * -kLog2e);
+      }
+    }
+    tm_st<CH>(tm + L::BETA + k, bx);
+    tm_st<CH>(tm + L::PB + k, pb);
+    tm_st<CH>(tm + L::MB + k, mb);
+    tm_st<CH>(tm + L::VB + k, vb);
+  }
+  float pt[1], mt[1], vt[1];
+  tm_ld<1>(tm + L::PT, pt);
+  tm_ld<1>(tm + L::MT, mt);
+  tm_ld<1>(tm + L::VT, vt);
+  tm_wait_ld();
+  tm_fence_regs(pt); tm_fence_regs(mt); tm_fence_regs(vt);
+  if (real && step) {
+    pt[0] = th;
+    if (ft) th = upd(th, dth, mt[0], vt[0], cfg.min_param);
+  } else if (real && rb) {
+    th = pt[0];
+  }
+  tm_st<1>(tm + L::PT, pt);
+  tm_st<1>(tm + L::MT, mt);
+  tm_st<1>(tm + L::VT, vt);
+  tm_wait_st();
 }
 
-template <int DP>
-__device__ __forceinline__ void store_params(const float2* A, const WarpCtx<DP>& c, int D,
-                                             int64_t w, float th, float* __restrict__ theta,
-                                             float* __restrict__ alpha, float* __restrict__ beta) {
-  if (c.j >= D) return;
-  theta[(size_t)w * D + c.j] = th;
-  for (int i = 0; i < D; i++) {
-    const float2 k = A[i * (DP + 1) + c.j];
-    alpha[(size_t)w * D * D + (size_t)i * D + c.j] = ab_alpha<DP>(i, k);
-    beta[(size_t)w * D * D + (size_t)i * D + c.j] = ab_beta<DP>(i, k);
+// Per-window (group-uniform) control of the fit loop (identical to
+// oracle_fit): decides the optimizer action after an evaluation and advances the counters.
+struct WinCtl {
+  int it = 0, s = 0, halv = 0, stall = 0, st = 0;
+  float lr_w = 0.0f;
+  double lnl_prev = 0.0;
+  bool have_prev = false, have_lnl = false;
+  // returns the action; sets done when the window stops
+  __device__ __forceinline__ int decide(const FitCfgDev& cfg, double lnl, bool finite, bool& done,
+                                        float* trace, int64_t w, bool lane0) {
+    int act = ACT_NONE;
+    if (!finite) {
+      st |= MDHP_ST_NONFINITE;
+      if (!have_prev || halv >= cfg.max_halvings) {
+        st |= MDHP_ST_DIVERGED;
+        done = true;
+        if (have_prev) act = ACT_ROLLBACK;
+      } else {
+        act = ACT_ROLLBACK;
+        lr_w *= 0.5f;
+        halv++;
+        it++;
+      }
+    } else {
+      if (trace && lane0) trace[(size_t)w * cfg.max_iters + it] = (float)lnl;
+      if (cfg.tol_rel > 0.0f && have_lnl) {
+        const double thr = (double)cfg.tol_rel * fmax(fabs(lnl_prev), 1.0);
+        stall = (fabs(lnl - lnl_prev) <= thr) ? stall + 1 : 0;
+        if (stall >= cfg.patience) {
+          st |= MDHP_ST_CONVERGED;
+          done = true;
+        }
+      }
+      if (!done) {
+        lnl_prev = lnl;
+        have_lnl = true;
+        have_prev = true;
+        s++;
+        act = ACT_STEP;
+        it++;
+      }
+    }
+    if (it >= cfg.max_iters) done = true;
+    return act;
   }
-}
+};
 
 // Persistent fit kernel (a6): windows are taken longest first from a global counter and run
-// their whole iteration loop on chip, then lnL is evaluated at the returned parameters and
-// everything is written back.
+// their whole iteration loop on chip (state in shared memory, optimizer state in TMEM), then
+// lnL is evaluated at the returned parameters and everything is written back.
 //   REFILL (converged mode, tol_rel > 0): each group of DP lanes takes one window at a time;
 //     when its window stops (convergence, divergence, budget) the group evaluates the final lnL,
 //     writes back and takes the next window at once, so a warp's other group(s) never idle
@@ -245,173 +492,116 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
       int32_t* __restrict__ xcount) {
   extern __shared__ __align__(16) unsigned char smem[];
   using SM = Smem<DP>;
+  using TL = TmCols<DP>;
   WarpCtx<DP> c;
   const int wid = threadIdx.x >> 5;
   float2* gbase_s = reinterpret_cast<float2*>(smem + wid * SM::per_warp) + c.g * SM::per_group;
   float2* A = gbase_s;
   float2* SQ = gbase_s + SM::AS;
   float2* Gs = gbase_s + 2 * SM::AS;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + (blockDim.x >> 5) * SM::per_warp);
+  const uint32_t tbase = tm_alloc(slot, TL::ALLOC);
+  const uint32_t tm = tbase + ((uint32_t)((wid & 3) * 32) << 16);
   const int D = P.D;
   if constexpr (REFILL) {
     enum { TRAIN = 0, FINAL = 1, IDLE = 2 };
-    // per-group (group-uniform) window and optimizer state
     int phase = IDLE;
     int64_t w = 0;
-    int st0 = 0, n = 0, it = 0, s = 0, halv = 0, stall = 0, st = 0;
-    bool live = false, have_prev = false, have_lnl = false;
-    float th = 0.0f, scale = 1.0f, lr_w = cfg.lr;
-    double lnl_prev = 0.0;
+    int st0 = 0, n = 0;
+    bool live = false;
+    float th = 0.0f, scale = 1.0f;
+    WinCtl ctl;
     ColInfo ci = col_info<DP>(P, 0, false, c.j);
-    // group-collective: take the next window (all lanes of the group, none of the others)
-    auto fetch = [&]() {
-      int64_t slot = 0;
-      if (c.j == 0) slot = atomicAdd(counter, 1);
-      slot = __shfl_sync(c.gmask, slot, c.gbase);
-      if (slot >= P.W) {
+    // group-collective: the next window index (all lanes of the group)
+    auto fetch = [&]() -> bool {
+      int64_t sl = 0;
+      if (c.j == 0) sl = atomicAdd(counter, 1);
+      sl = __shfl_sync(c.gmask, sl, c.gbase);
+      if (sl >= P.W) {
         phase = IDLE;
         live = false;
         n = 0;
-        return;
+        return false;
       }
-      w = P.perm[slot];
+      w = P.perm[sl];
       MDHP_ASSERT(w >= 0 && w < P.W);
       st0 = status[w];
       live = !(st0 & MDHP_ST_INVALID);
-      th = load_params<DP>(A, c, D, w, live, theta, alpha, beta);
       ci = col_info<DP>(P, w, live, c.j);
       n = live ? P.n[w] : 0;
       scale = (cfg.loss_mean && n > 0) ? 1.0f / (float)n : 1.0f;
-      it = s = halv = stall = st = 0;
-      lr_w = cfg.lr;
-      lnl_prev = 0.0;
-      have_prev = have_lnl = false;
+      ctl = WinCtl();
+      ctl.lr_w = cfg.lr;
       phase = (!live || cfg.max_iters <= 0) ? FINAL : TRAIN;
+      return true;
     };
-    fetch();
+    bool got = fetch();
+    th = load_window<DP>(A, c, D, w, got, live, tm, th, theta, alpha, beta, opt);
     while (__any_sync(kFull, phase != IDLE)) {
-      const bool act = phase != IDLE && live;
-      const int nmax = group_max_i<DP>(act ? n : 0);
+      const bool act_eval = phase != IDLE && live;
+      const int nmax = group_max_i<DP>(act_eval ? n : 0);
       float dth;
       bool finite, exact;
       // gradients only when some group trains (a warp whose groups all stop together, as in the
       // fixed-iteration mode, evaluates its final lnL without them)
       const double lnl = __any_sync(kFull, phase == TRAIN)
-                             ? eval_window<DP, true>(P, A, SQ, Gs, c, w, act, nmax, th, ci, dth, finite, exact)
-                             : eval_window<DP, false>(P, A, SQ, Gs, c, w, act, nmax, th, ci, dth, finite, exact);
+                             ? eval_window<DP, true>(P, A, SQ, Gs, c, w, act_eval, nmax, th, ci, dth, finite, exact)
+                             : eval_window<DP, false>(P, A, SQ, Gs, c, w, act_eval, nmax, th, ci, dth, finite, exact);
+      int act = ACT_NONE;
+      bool fin = false;
       if (phase == TRAIN) {
         bool done = false;
-        if (!finite) {
-          st |= MDHP_ST_NONFINITE;
-          if (!have_prev || halv >= cfg.max_halvings) {
-            st |= MDHP_ST_DIVERGED;
-            done = true;
-            if (have_prev) th = load_params<DP>(A, c, D, w, true, theta, alpha, beta);
-          } else {
-            th = load_params<DP>(A, c, D, w, true, theta, alpha, beta);
-            lr_w *= 0.5f;
-            halv++;
-            it++;
-          }
-        } else {
-          if (trace && c.j == 0) trace[(size_t)w * cfg.max_iters + it] = (float)lnl;
-          if (cfg.tol_rel > 0.0f && have_lnl) {
-            const double thr = (double)cfg.tol_rel * fmax(fabs(lnl_prev), 1.0);
-            stall = (fabs(lnl - lnl_prev) <= thr) ? stall + 1 : 0;
-            if (stall >= cfg.patience) {
-              st |= MDHP_ST_CONVERGED;
-              done = true;
-            }
-          }
-          if (!done) {
-            lnl_prev = lnl;
-            have_lnl = true;
-            store_params<DP>(A, c, D, w, th, theta, alpha, beta);   // previous point
-            have_prev = true;
-            s++;
-            step_column<DP, RESUME>(A, Gs, c, D, w, cfg, lr_w, s, scale, dth, th, opt);
-            it++;
-          }
-        }
-        if (it >= cfg.max_iters) done = true;
+        act = ctl.decide(cfg, lnl, finite, done, trace, w, c.j == 0);
         if (done) phase = FINAL;   // the next evaluation is lnL at the returned parameters
       } else if (phase == FINAL) {
-        if (live) store_params<DP>(A, c, D, w, th, theta, alpha, beta);
+        fin = true;
         if (c.j == 0) {
           lnl_out[w] = live ? lnl : (double)NAN;
-          iters_out[w] = it;
-          status[w] = (st0 & kKeepStatus) | st;
+          iters_out[w] = ctl.it;
+          status[w] = (st0 & kKeepStatus) | ctl.st;
           if (exact) list_exact(xlist, xcount, w);
           if (trace && live)
-            for (int q = it; q < cfg.max_iters; q++) trace[(size_t)w * cfg.max_iters + q] = NAN;
+            for (int q = ctl.it; q < cfg.max_iters; q++) trace[(size_t)w * cfg.max_iters + q] = NAN;
         }
-        fetch();
+      }
+      if (__any_sync(kFull, act != ACT_NONE))
+        opt_action<DP, RESUME>(A, Gs, c, D, cfg, act, ctl.lr_w, ctl.s, scale, dth, th, tm);
+      if (__any_sync(kFull, fin)) {
+        store_window<DP>(A, c, D, w, fin && live, th, tm, theta, alpha, beta, opt);
+        bool nw = false;
+        if (fin) nw = fetch();
+        th = load_window<DP>(A, c, D, w, nw, live, tm, th, theta, alpha, beta, opt);
       }
       __syncwarp();
     }
   } else {
-    // fixed iteration count: every window of a warp stops at the same evaluation, so the
-    // warp keeps its G windows to the end (no per-window refill bookkeeping)
     const int64_t nunits = (P.W + SM::G - 1) / SM::G;
     for (;;) {
       int64_t unit = 0;
       if (c.lane == 0) unit = atomicAdd(counter, 1);
       unit = __shfl_sync(kFull, unit, 0);
       if (unit >= nunits) break;
-      const int64_t slot = unit * SM::G + c.g;
-      const int64_t w = slot < P.W ? P.perm[slot] : 0;
+      const int64_t slot_w = unit * SM::G + c.g;
+      const int64_t w = slot_w < P.W ? P.perm[slot_w] : 0;
       MDHP_ASSERT(w >= 0 && w < (P.W > 0 ? P.W : 1));
-      const int st0 = slot < P.W ? status[w] : MDHP_ST_INVALID;
-      const bool live = slot < P.W && !(st0 & MDHP_ST_INVALID);
-      float th = load_params<DP>(A, c, D, w, live, theta, alpha, beta);
+      const int st0 = slot_w < P.W ? status[w] : MDHP_ST_INVALID;
+      const bool live = slot_w < P.W && !(st0 & MDHP_ST_INVALID);
+      float th = load_window<DP>(A, c, D, w, true, live, tm, 0.0f, theta, alpha, beta, opt);
       const ColInfo ci = col_info<DP>(P, w, live, c.j);
       const int n = live ? P.n[w] : 0;
       const float scale = (cfg.loss_mean && n > 0) ? 1.0f / (float)n : 1.0f;
-      // per-window (group-uniform) optimizer state
-      int it = 0, s = 0, halv = 0, stall = 0, st = 0;
-      float lr_w = cfg.lr;
-      double lnl_prev = 0.0;
-      bool have_prev = false, have_lnl = false;
+      WinCtl ctl;
+      ctl.lr_w = cfg.lr;
       bool done = !live || cfg.max_iters <= 0;
       while (__any_sync(kFull, !done)) {
         const int nmax = group_max_i<DP>(done ? 0 : n);
         float dth;
         bool finite, exact;
         const double lnl = eval_window<DP, true>(P, A, SQ, Gs, c, w, !done, nmax, th, ci, dth, finite, exact);
-        if (!done) {
-          if (!finite) {
-            st |= MDHP_ST_NONFINITE;
-            if (!have_prev || halv >= cfg.max_halvings) {
-              st |= MDHP_ST_DIVERGED;
-              done = true;
-              if (have_prev) th = load_params<DP>(A, c, D, w, true, theta, alpha, beta);
-            } else {
-              th = load_params<DP>(A, c, D, w, true, theta, alpha, beta);
-              lr_w *= 0.5f;
-              halv++;
-              it++;
-            }
-          } else {
-            if (trace && c.j == 0) trace[(size_t)w * cfg.max_iters + it] = (float)lnl;
-            if (cfg.tol_rel > 0.0f && have_lnl) {
-              const double thr = (double)cfg.tol_rel * fmax(fabs(lnl_prev), 1.0);
-              stall = (fabs(lnl - lnl_prev) <= thr) ? stall + 1 : 0;
-              if (stall >= cfg.patience) {
-                st |= MDHP_ST_CONVERGED;
-                done = true;
-              }
-            }
-            if (!done) {
-              lnl_prev = lnl;
-              have_lnl = true;
-              store_params<DP>(A, c, D, w, th, theta, alpha, beta);   // previous point
-              have_prev = true;
-              s++;
-              step_column<DP, RESUME>(A, Gs, c, D, w, cfg, lr_w, s, scale, dth, th, opt);
-              it++;
-            }
-          }
-          if (it >= cfg.max_iters) done = true;
-        }
+        int act = ACT_NONE;
+        if (!done) act = ctl.decide(cfg, lnl, finite, done, trace, w, c.j == 0);
+        if (__any_sync(kFull, act != ACT_NONE))
+          opt_action<DP, RESUME>(A, Gs, c, D, cfg, act, ctl.lr_w, ctl.s, scale, dth, th, tm);
         __syncwarp();
       }
       // lnL at the returned parameters (no gradient accumulation needed)
@@ -419,20 +609,19 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
       float dth;
       bool finite, exact;
       const double lnl = eval_window<DP, false>(P, A, SQ, Gs, c, w, live, nmax, th, ci, dth, finite, exact);
-      if (slot < P.W) {
-        if (live) store_params<DP>(A, c, D, w, th, theta, alpha, beta);
-        if (c.j == 0) {
-          lnl_out[w] = live ? lnl : (double)NAN;
-          iters_out[w] = it;
-          status[w] = (st0 & kKeepStatus) | st;
-          if (exact) list_exact(xlist, xcount, w);
-          if (trace && live)
-            for (int q = it; q < cfg.max_iters; q++) trace[(size_t)w * cfg.max_iters + q] = NAN;
-        }
+      store_window<DP>(A, c, D, w, slot_w < P.W && live, th, tm, theta, alpha, beta, opt);
+      if (slot_w < P.W && c.j == 0) {
+        lnl_out[w] = live ? lnl : (double)NAN;
+        iters_out[w] = ctl.it;
+        status[w] = (st0 & kKeepStatus) | ctl.st;
+        if (exact) list_exact(xlist, xcount, w);
+        if (trace && live)
+          for (int q = ctl.it; q < cfg.max_iters; q++) trace[(size_t)w * cfg.max_iters + q] = NAN;
       }
       __syncwarp();
     }
   }
+  tm_free(tbase, TL::ALLOC);
 }
 
 // ---------------------------------------------------------------- host launchers
@@ -478,7 +667,7 @@ static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float*
                         int* counter, int32_t* xlist, int32_t* xcount, cudaStream_t st) {
   using SM = Smem<DP>;
   constexpr int WPB = 4;
-  const size_t smem = WPB * SM::per_warp;
+  const size_t smem = WPB * SM::per_warp + 16;   // + the TMEM base address slot
   // converged mode (tol_rel > 0): windows stop at different iterations -> per-window refill
   auto kern = cfg.tol_rel > 0.0f ? (cfg.step0 != 0 ? k_fit<DP, true, true> : k_fit<DP, false, true>)
                                  : (cfg.step0 != 0 ? k_fit<DP, true, false> : k_fit<DP, false, false>);
@@ -490,7 +679,27 @@ static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float*
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem);
+  // CTAs per SM from registers, shared memory and TMEM columns.  (The occupancy API reports 1
+  // for kernels that allocate tensor memory; the hardware runs as many as the resources allow
+  // and tcgen05.alloc would wait for columns, so the grid is sized from the resources here.)
+  cudaFuncAttributes fa;
+  int smem_sm = 0, smem_rsv = 0;
+  if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess ||
+      cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess) {
+    set_error("k_fit: device attribute query failed");
+    return MDHP_ECUDA;
+  }
+  const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+  const int by_regs = 65536 / (regs_warp * WPB);
+  const int by_smem = smem_sm / (int)(smem + fa.sharedSizeBytes + smem_rsv);
+  const int by_tmem = 512 / (int)TmCols<DP>::ALLOC;
+  per_sm = by_regs < by_smem ? by_regs : by_smem;
+  if (per_sm > by_tmem) per_sm = by_tmem;
+  if (per_sm > 2048 / (WPB * 32)) per_sm = 2048 / (WPB * 32);
+  if (getenv("MDHP_DEBUG_LAUNCH"))
+    fprintf(stderr, "k_fit<%d>: per_sm=%d (regs %d smem %d tmem %d) smem=%zu regs=%d local=%zu\n", DP,
+            per_sm, by_regs, by_smem, by_tmem, smem, fa.numRegs, fa.localSizeBytes);
   if (per_sm < 1) per_sm = 1;
   const int64_t units = (P.W + SM::G - 1) / SM::G;
   int64_t blocks = (int64_t)sms * per_sm;

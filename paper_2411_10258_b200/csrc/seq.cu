@@ -595,10 +595,10 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
   // anchored at their base (relative time 0; their events are strictly later, R2/R10)
   const float last0 = (c == 0 && !has_history) ? -1.0f : 0.0f;
   if (grad)
-    event_loop<DP, true>(A, SQ, Gs, j, gbase, t32, dtp, mk, live ? cbeg[c] : 0, n, nmax, th, last,
+    event_loop<DP, true, false>(A, SQ, Gs, j, gbase, t32, dtp, mk, live ? cbeg[c] : 0, n, nmax, th, last,
                          gth, lsum, last0);
   else
-    event_loop<DP, false>(A, SQ, Gs, j, gbase, t32, dtp, mk, live ? cbeg[c] : 0, n, nmax, th,
+    event_loop<DP, false, false>(A, SQ, Gs, j, gbase, t32, dtp, mk, live ? cbeg[c] : 0, n, nmax, th,
                           last, gth, lsum, last0);
   lsum = group_sum_d<DP>(lsum);
   // Phase 4a, first stage, fused: the block's 4G chunks are summed in a fixed order (fp64) into
