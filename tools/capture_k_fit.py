@@ -59,7 +59,8 @@ def parse(path):
     W, E = cfgj["windows"], cfgj["per_rank"]["events"][0]
     evals = cfgj["iterations"] + 1
     ev_eval = cfgj["event_evaluations_per_step"]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "B": 1, "KB": 1e3, "MB": 1e6,
+             "GB": 1e9, "TB": 1e12}
     b = lambda k: vals[k] * scale.get(units[k], 1.0)
     dram = b("dram__bytes_read.sum") + b("dram__bytes_write.sum")
     lts = b("lts__t_bytes.sum")
@@ -70,8 +71,8 @@ def parse(path):
     shfl_per_ev = 9 / 16
     mio = (wf + shfl_per_ev * ev_eval) / (148 * cyc)
     out = {"kernel": kernel.split("(")[0], "source_hash": bench.source_hash(), "windows": W, "events": E,
-           "evaluations": evals, "event_evaluations": ev_eval, "gpu_time_s": vals["gpu__time_duration.sum"] * (
-               1e-9 if units["gpu__time_duration.sum"] == "nsecond" else 1e-6 if units["gpu__time_duration.sum"] == "usecond" else 1e-3),
+           "evaluations": evals, "event_evaluations": ev_eval, "gpu_time_s": vals["gpu__time_duration.sum"] * {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6,
+                                                            "ms": 1e-3, "msecond": 1e-3}[units["gpu__time_duration.sum"]],
            "dram_bytes": dram, "dram_bytes_per_event_evaluation": dram / ev_eval, "l2_bytes": lts,
            "shared_wavefronts": wf, "shared_wavefronts_per_event_evaluation": wf / ev_eval,
            "bank_conflicts": vals.get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
