@@ -45,12 +45,35 @@ __constant__ float c_inv_fact[kMom + 1] = {
 template <int DP>
 struct Smem {
   static constexpr int G = 32 / DP;                 // windows (groups) per warp
-  static constexpr int RS = DP + 1;                 // row stride of A and SQ (float2 units)
-  static constexpr int AS = (DP + 1) * RS;          // float2 per group in A (and in SQ): DP real
-                                                    // rows + the null row DP
-  static constexpr int GS = (DP + 1) * DP;          // float2 per group in G (+ null row)
-  static constexpr int per_group = 2 * AS + GS;     // float2
-  static constexpr size_t per_warp = (size_t)G * per_group * sizeof(float2);
+  // DP >= 16: each group owns (DP+1) x (DP+1) arrays with odd row stride DP+1 (row and column
+  //   accesses of a group's 16 or 32 lanes are conflict-free).
+  // DP <= 8 (SW, swizzled): the 16/DP groups of a half-warp share rows of 16 float2 (128 B):
+  //   group h of the half-warp owns float2 DP*h .. DP*h+DP-1 of every row, and element (r, c)
+  //   sits at 16 r + ((c ^ r) & (DP-1)) from the group's base, so a row read (lanes c) and a
+  //   column access (lanes r) of each group hit DP distinct 8-byte bank pairs inside the
+  //   group's own half of the 16 pairs: 64-bit accesses of a half-warp are conflict-free
+  //   whatever the groups' marks (the odd-stride layout measured 46% excess wavefronts at
+  //   DP = 8, profiles/r02_cfg2_*).  The null column (index DP) has no storage there: the
+  //   event loop never stores to it and nothing reads it.
+  static constexpr bool SW = DP <= 8;
+  static constexpr int RS = SW ? 16 : DP + 1;       // row stride of A and SQ (float2 units)
+  static constexpr int AS = (DP + 1) * RS;          // float2 from A to SQ (and SQ to G): DP
+                                                    // real rows + the null row DP
+  static constexpr int GS = SW ? AS : (DP + 1) * DP;   // float2 of G (+ null row)
+  static constexpr int P = SW ? 16 / DP : 1;        // groups sharing one row block
+  static constexpr int per_group = 2 * AS + GS;     // float2 per group (SW: per block of P)
+  static constexpr size_t per_warp = (size_t)(G / P) * per_group * sizeof(float2);
+  // float2 offset of group g's A from the warp's base
+  __host__ __device__ static constexpr int group_off(int g) {
+    return SW ? (g / P) * per_group + (g % P) * DP : g * per_group;
+  }
+  // float2 offset of element (r, c) of A / SQ (e) and of G (ge) from the array base
+  __host__ __device__ static constexpr int e(int r, int c) {
+    return SW ? r * 16 + ((c ^ r) & (DP - 1)) : r * (DP + 1) + c;
+  }
+  __host__ __device__ static constexpr int ge(int r, int c) {
+    return SW ? r * 16 + ((c ^ r) & (DP - 1)) : r * DP + c;
+  }
 };
 
 // Parameter pair order in A.  Half of the pairs are stored {beta, alpha} instead of
@@ -91,13 +114,14 @@ constexpr float kNullT = -2.0f;
 // null column; (re)set the null row.
 template <int DP>
 __device__ __forceinline__ void reset_state(float2* SQ, float2* Gs, int j) {
+  using SM = Smem<DP>;
 #pragma unroll
   for (int i = 0; i < DP; i++) {
-    SQ[i * (DP + 1) + j] = make_float2(0.0f, 0.0f);
-    Gs[i * DP + j] = make_float2(0.0f, 0.0f);
+    SQ[SM::e(i, j)] = make_float2(0.0f, 0.0f);
+    Gs[SM::ge(i, j)] = make_float2(0.0f, 0.0f);
   }
-  SQ[DP * (DP + 1) + j] = make_float2(j == 0 ? 1.0f : 0.0f, 0.0f);
-  SQ[j * (DP + 1) + DP] = make_float2(0.0f, 0.0f);
+  SQ[SM::e(DP, j)] = make_float2(j == 0 ? 1.0f : 0.0f, 0.0f);
+  if constexpr (!SM::SW) SQ[SM::e(j, DP)] = make_float2(0.0f, 0.0f);
 }
 
 // Reduce-scatter of 8 per-lane values v[0..7] over the DP lanes of a group (DP >= 8): on
@@ -253,15 +277,19 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
                                               float2* __restrict__ SQ, float2* __restrict__ Gs,
                                               const int j, const int gbase, const float th,
                                               float& last, float& gth, double& lsum) {
-  constexpr int RS = DP + 1;
+  using SM = Smem<DP>;
+  constexpr bool SW = SM::SW;
+  constexpr int RS = SM::RS;
   constexpr int LG = Log2<DP>::v;
-  constexpr int kSQ = Smem<DP>::AS * 8, kG = 2 * Smem<DP>::AS * 8;   // byte offsets from A
-  MDHP_ASSERT(SQ == A + Smem<DP>::AS && Gs == A + 2 * Smem<DP>::AS);
+  constexpr int kSQ = SM::AS * 8, kG = 2 * SM::AS * 8;   // byte offsets from A
+  MDHP_ASSERT(SQ == A + SM::AS && Gs == A + 2 * SM::AS);
   const uint32_t sA = static_cast<uint32_t>(__cvta_generic_to_shared(A));
-  // per-lane bases: row i of column j at rowb + i*RS*8, column i of row j at colb + i*8,
-  // gradient row i of column j at rowb + kG + i*DP*8
-  const uint32_t rowb = sA + 8u * j;
-  const uint32_t colb = sA + 8u * RS * j;
+  // per-lane bases.  Odd stride: row i of column j at rowb + i*RS*8, column i of row j at
+  // colb + i*8, gradient row i of column j at rowb + kG + i*DP*8.  SW: element (r, c) at
+  // sA + 128 r + 8 x with x = (c ^ r) & (DP-1); the row read (i, j) and the column access
+  // (j, i) of an event share x = (i ^ j) & (DP-1); gradients at the row-read address + kG.
+  const uint32_t rowb = SW ? sA : sA + 8u * j;
+  const uint32_t colb = SW ? sA + 128u * j : sA + 8u * RS * j;
   // beta of a column pair: word 1, or word 0 where the pair is stored swapped
   const uint32_t colbb = colb + (ab_swapped<DP>(j) ? 0u : 4u);
   float pv[8], Rv[8], Qv[8];
@@ -275,13 +303,21 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
     const int i = (int)__byte_perm(word, 0u, 0x4440u | (unsigned)(s & 3));   // mark (null: DP)
     MDHP_ASSERT(i >= 0 && i <= DP);
-    const uint32_t ra = rowb + (uint32_t)i * (8u * RS);
-    const uint32_t ca = colb + ((uint32_t)i << 3);
-    MDHP_ASSERT(ra + kSQ + 8 <= sA + 8u * Smem<DP>::per_group &&
-                ca + kSQ + 4 <= sA + 8u * Smem<DP>::per_group);
+    uint32_t ra, ca, cab;
+    if constexpr (SW) {
+      const uint32_t x = ((uint32_t)(i ^ j) & (uint32_t)(DP - 1)) << 3;
+      ra = sA + (uint32_t)i * 128u + x;
+      ca = colb + x;
+      cab = colbb + x;
+    } else {
+      ra = rowb + (uint32_t)i * (8u * RS);
+      ca = colb + ((uint32_t)i << 3);
+      cab = colbb + ((uint32_t)i << 3);
+    }
+    MDHP_ASSERT(ra + kG + 8 <= sA + 8u * (uint32_t)(3 * SM::AS) && ca + kSQ + 8 <= sA + 8u * (uint32_t)(3 * SM::AS));
     const float2 ar = lda2(ra);
     const float2 sr = lds2o<kSQ>(ra);
-    const float bc = lda1o<0>(colbb + ((uint32_t)i << 3));
+    const float bc = lda1o<0>(cab);
     const float2 sc = lds2o<kSQ>(ca);
     const float dr = t - last;
     const float a_ij = ab_alpha<DP>(i, ar), b_ij = ab_beta<DP>(i, ar);
@@ -290,7 +326,8 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     const float R = fmaf(er, sr.x, -fset_eq0(dr));   // strict T_j^k < t
     // theta_i enters after the reduction for DP >= 8 (below), through lane i for DP <= 4
     const float p = DP >= 8 ? a_ij * R : fmaf(a_ij, R, fsel_eqi(i, j, th, 0.0f));
-    sts2o<kSQ>(ca, fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
+    // SW: the null column has no storage; a null event's column update is not stored
+    if (!SW || i < DP) sts2o<kSQ>(ca, fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
     last = fsel_eqi(i, j, t, last);
     if constexpr (DP >= 8) {
       pv[s] = p;
@@ -302,8 +339,8 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
       const float lam = group_sum<DP>(p);
       if (GRAD) {
         const float w = rcpf(lam);
-        const uint32_t ga = rowb + ((uint32_t)i * (8u * DP));
-        MDHP_ASSERT(ga + kG + 8 <= sA + 8u * Smem<DP>::per_group);
+        const uint32_t ga = SW ? ra : rowb + ((uint32_t)i * (8u * DP));
+        MDHP_ASSERT(ga + kG + 8 <= sA + 8u * (uint32_t)(3 * SM::AS));
         const float2 gg = lds2o<kG>(ga);
         sts2o<kG>(ga, fmaf(R, w, gg.x), fmaf(er * fmaf(dr, sr.x, sr.y), w, gg.y));
         gth += fsel_eqi(i, j, w, 0.0f);
@@ -335,7 +372,7 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
       // (DP <= 16; for DP = 32, one window per warp, the shuffles measured faster).
       float4 wa = make_float4(0.f, 0.f, 0.f, 0.f), wb = wa;
       if constexpr (DP <= 16) {
-        const uint32_t scr = sA + kG + 8u * DP * DP;
+        const uint32_t scr = sA + kG + (SW ? 128u * DP : 8u * DP * DP);   // G's null row
         if ((j & ((DP >> 3) - 1)) == 0) sts1(scr + 4u * e, w);
         __syncwarp();
         wa = lds4(scr);
@@ -352,8 +389,9 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
         // register with two LOP3 each)
         const int i = (int)((word >> (8 * (s & 3))) & 0xffu);
         MDHP_ASSERT(i >= 0 && i <= DP);
-        const uint32_t ga = (rowb + kG) + ((uint32_t)i << (3 + LG));
-        MDHP_ASSERT(ga >= sA + kG && ga + 8 <= sA + 8u * Smem<DP>::per_group);
+        const uint32_t ga = SW ? (sA + kG) + (uint32_t)i * 128u + (((uint32_t)(i ^ j) & (uint32_t)(DP - 1)) << 3)
+                               : (rowb + kG) + ((uint32_t)i << (3 + LG));
+        MDHP_ASSERT(ga >= sA + kG && ga + 8 <= sA + 8u * (uint32_t)(3 * SM::AS));
         const float2 gg = lds2(ga);
         sts2o<0>(ga, fmaf(Rv[s], ws, gg.x), fmaf(Qv[s], ws, gg.y));
         gth += fsel_eqi(i, j, ws, 0.0f);

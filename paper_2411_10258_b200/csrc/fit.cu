@@ -47,6 +47,7 @@ __device__ __forceinline__ double eval_window(const Packed& P, float2* A, float2
                                               const WarpCtx<DP>& c, int64_t w, bool live,
                                               int nmax, float th, const ColInfo& ci,
                                               float& dth, bool& finite, bool& exact) {
+  using SM = Smem<DP>;
   reset_state<DP>(SQ, Gs, c.j);
   __syncwarp();
   const int n = live ? P.n[w] : 0;
@@ -63,8 +64,8 @@ __device__ __forceinline__ double eval_window(const Packed& P, float2* A, float2
   bool ok = true;
 #pragma unroll 4
   for (int i = 0; i < DP; i++) {
-    const float2 k = A[i * (DP + 1) + c.j];
-    const float2 sq = SQ[i * (DP + 1) + c.j];
+    const float2 k = A[SM::e(i, c.j)];
+    const float2 sq = SQ[SM::e(i, c.j)];
     float Eb, Hb2;
     // A holds beta' = -beta log2 e; the compensator takes beta (one rounding of beta' * -ln 2)
     const float ka = ab_alpha<DP>(i, k), kb = ab_beta<DP>(i, k) * -kLn2;
@@ -72,11 +73,11 @@ __device__ __forceinline__ double eval_window(const Packed& P, float2* A, float2
     if (cc.real && i < P.D) {
       part3 += (double)(ka * Eb);
       if (GRAD) {
-        float2 gg = Gs[i * DP + c.j];
+        float2 gg = Gs[SM::ge(i, c.j)];
         const float da = gg.x + Eb;
         const float db = fmaf(-ka, gg.y, ka * Hb2);
         ok = ok && isfinite(da) && isfinite(db);
-        Gs[i * DP + c.j] = make_float2(da, db);
+        Gs[SM::ge(i, c.j)] = make_float2(da, db);
       }
     }
   }
@@ -110,6 +111,7 @@ __device__ __forceinline__ float load_params(float2* A, const WarpCtx<DP>& c, in
                                              bool live, const float* __restrict__ theta,
                                              const float* __restrict__ alpha,
                                              const float* __restrict__ beta) {
+  using SM = Smem<DP>;
   const bool real = live && c.j < D;
 #pragma unroll 4
   for (int i = 0; i < DP; i++) {
@@ -118,11 +120,11 @@ __device__ __forceinline__ float load_params(float2* A, const WarpCtx<DP>& c, in
       a = alpha[(size_t)w * D * D + (size_t)i * D + c.j];
       b = beta[(size_t)w * D * D + (size_t)i * D + c.j];
     }
-    A[i * (DP + 1) + c.j] = ab_pack<DP>(i, a, b * -kLog2e);
+    A[SM::e(i, c.j)] = ab_pack<DP>(i, a, b * -kLog2e);
   }
   // null dimension (see eval.cuh): row DP = {1,0} at column 0, column DP has beta = 0
-  A[DP * (DP + 1) + c.j] = ab_pack<DP>(DP, c.j == 0 ? 1.0f : 0.0f, 0.0f);
-  A[c.j * (DP + 1) + DP] = make_float2(0.0f, 0.0f);
+  A[SM::e(DP, c.j)] = ab_pack<DP>(DP, c.j == 0 ? 1.0f : 0.0f, 0.0f);
+  if constexpr (!SM::SW) A[SM::e(c.j, DP)] = make_float2(0.0f, 0.0f);
   return real ? theta[(size_t)w * D + c.j] : 0.0f;
 }
 
@@ -137,7 +139,7 @@ k_loglik(Packed P, const float* __restrict__ theta, const float* __restrict__ al
   using SM = Smem<DP>;
   WarpCtx<DP> c;
   const int wid = threadIdx.x >> 5;
-  float2* gbase_s = reinterpret_cast<float2*>(smem + wid * SM::per_warp) + c.g * SM::per_group;
+  float2* gbase_s = reinterpret_cast<float2*>(smem + wid * SM::per_warp) + SM::group_off(c.g);
   float2* A = gbase_s;
   float2* SQ = gbase_s + SM::AS;
   float2* Gs = gbase_s + 2 * SM::AS;
@@ -163,7 +165,7 @@ k_loglik(Packed P, const float* __restrict__ theta, const float* __restrict__ al
   if (grad && c.j < D) {
     g_theta[(size_t)w * D + c.j] = live ? dth : NAN;
     for (int i = 0; i < D; i++) {
-      const float2 gg = Gs[i * DP + c.j];
+      const float2 gg = Gs[SM::ge(i, c.j)];
       g_alpha[(size_t)w * D * D + (size_t)i * D + c.j] = live ? gg.x : NAN;
       g_beta[(size_t)w * D * D + (size_t)i * D + c.j] = live ? gg.y : NAN;
     }
@@ -197,6 +199,7 @@ __device__ __forceinline__ float load_window(float2* A, const WarpCtx<DP>& c, in
                                              const float* __restrict__ alpha,
                                              const float* __restrict__ beta,
                                              const float* __restrict__ opt) {
+  using SM = Smem<DP>;
   using L = TmCols<DP>;
   constexpr int CH = L::CH;
   const bool real = load && live && c.j < D;
@@ -223,7 +226,7 @@ __device__ __forceinline__ float load_window(float2* A, const WarpCtx<DP>& c, in
           a = alpha[(size_t)w * D * D + (size_t)i * D + c.j];
           b = beta[(size_t)w * D * D + (size_t)i * D + c.j];
         }
-        A[i * (DP + 1) + c.j] = ab_pack<DP>(i, a, b * -kLog2e);
+        A[SM::e(i, c.j)] = ab_pack<DP>(i, a, b * -kLog2e);
         bx[u] = b;
         const size_t qa = (size_t)D + (size_t)i * D + c.j, qb = qa + (size_t)D * D;
         ma[u] = (m && r) ? m[qa] : 0.0f;
@@ -249,8 +252,8 @@ __device__ __forceinline__ float load_window(float2* A, const WarpCtx<DP>& c, in
     vt[0] = v ? v[c.j] : 0.0f;
     th = real ? theta[(size_t)w * D + c.j] : 0.0f;
     // null dimension (see eval.cuh): row DP = {1,0} at column 0, column DP has beta = 0
-    A[DP * (DP + 1) + c.j] = ab_pack<DP>(DP, c.j == 0 ? 1.0f : 0.0f, 0.0f);
-    A[c.j * (DP + 1) + DP] = make_float2(0.0f, 0.0f);
+    A[SM::e(DP, c.j)] = ab_pack<DP>(DP, c.j == 0 ? 1.0f : 0.0f, 0.0f);
+    if constexpr (!SM::SW) A[SM::e(c.j, DP)] = make_float2(0.0f, 0.0f);
   }
   tm_st<1>(tm + L::MT, mt);
   tm_st<1>(tm + L::VT, vt);
@@ -266,6 +269,7 @@ __device__ __forceinline__ void store_window(const float2* A, const WarpCtx<DP>&
                                              int64_t w, bool store, float th, uint32_t tm,
                                              float* __restrict__ theta, float* __restrict__ alpha,
                                              float* __restrict__ beta, float* __restrict__ opt) {
+  using SM = Smem<DP>;
   using L = TmCols<DP>;
   constexpr int CH = L::CH;
   const bool real = store && c.j < D;
@@ -287,7 +291,7 @@ __device__ __forceinline__ void store_window(const float2* A, const WarpCtx<DP>&
       const int i = k + u;
       if (real && i < D) {
         const size_t q = (size_t)w * D * D + (size_t)i * D + c.j;
-        alpha[q] = ab_alpha<DP>(i, A[i * (DP + 1) + c.j]);
+        alpha[q] = ab_alpha<DP>(i, A[SM::e(i, c.j)]);
         beta[q] = bx[u];
         if (m) {
           const size_t qa = (size_t)D + (size_t)i * D + c.j, qb = qa + (size_t)D * D;
@@ -320,6 +324,7 @@ template <int DP, bool RESUME>
 __device__ __forceinline__ void opt_action(float2* A, const float2* Gs, const WarpCtx<DP>& c,
                                            int D, const FitCfgDev& cfg, int act, float lr_w,
                                            int s, float scale, float dth, float& th, uint32_t tm) {
+  using SM = Smem<DP>;
 #ifdef MDHP_AB_NO_OPT
   return;   // A/B timing probe only: no optimizer action
 #endif
@@ -363,11 +368,11 @@ __device__ __forceinline__ void opt_action(float2* A, const float2* Gs, const Wa
     for (int u = 0; u < CH; u++) {
       const int i = k + u;
       if (real && i < D && act != ACT_NONE) {
-        float2* e = &A[i * (DP + 1) + c.j];
+        float2* e = &A[SM::e(i, c.j)];
         float a = ab_alpha<DP>(i, *e);
         if (step) {
           pa[u] = a;
-          if (fa) a = upd(a, Gs[i * DP + c.j].x, ma[u], va[u], 0.0f);
+          if (fa) a = upd(a, Gs[SM::ge(i, c.j)].x, ma[u], va[u], 0.0f);
         } else {
           a = pa[u];
         }
@@ -394,12 +399,12 @@ __device__ __forceinline__ void opt_action(float2* A, const float2* Gs, const Wa
         float b = bx[u];
         if (step) {
           pb[u] = b;
-          if (fb) b = upd(b, Gs[i * DP + c.j].y, mb[u], vb[u], cfg.min_param);
+          if (fb) b = upd(b, Gs[SM::ge(i, c.j)].y, mb[u], vb[u], cfg.min_param);
         } else {
           b = pb[u];
         }
         bx[u] = b;
-        float2* e = &A[i * (DP + 1) + c.j];
+        float2* e = &A[SM::e(i, c.j)];
         *e = ab_pack<DP>(i, ab_alpha<DP>(i, *e), b * -kLog2e);
       }
     }
@@ -495,7 +500,7 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
   using TL = TmCols<DP>;
   WarpCtx<DP> c;
   const int wid = threadIdx.x >> 5;
-  float2* gbase_s = reinterpret_cast<float2*>(smem + wid * SM::per_warp) + c.g * SM::per_group;
+  float2* gbase_s = reinterpret_cast<float2*>(smem + wid * SM::per_warp) + SM::group_off(c.g);
   float2* A = gbase_s;
   float2* SQ = gbase_s + SM::AS;
   float2* Gs = gbase_s + 2 * SM::AS;

@@ -552,10 +552,9 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
   if (ctl && ctl[0] == 1 && grad) return;
   extern __shared__ __align__(16) unsigned char smem[];
   using SM = Smem<DP>;
-  constexpr int RS = DP + 1;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / DP, j = lane % DP;
   const int gbase = g * DP;
-  float2* base = reinterpret_cast<float2*>(smem + wid * SM::per_warp) + g * SM::per_group;
+  float2* base = reinterpret_cast<float2*>(smem + wid * SM::per_warp) + SM::group_off(g);
   float2* A = base;
   float2* SQ = base + SM::AS;
   float2* Gs = base + 2 * SM::AS;
@@ -566,24 +565,26 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
   // trip at the wait below instead of one per row: this prologue was ~15% of the kernel)
   for (int i = 0; i < DP; i++) {
     const bool real = live && i < D && j < D;
-    float2* a = &A[i * RS + j];
+    float2* a = &A[SM::e(i, j)];
     if (real) {
       float* af = reinterpret_cast<float*>(a);
       const bool sw = ab_swapped<DP>(i);
       cp_async<4>(af + (sw ? 1 : 0), alpha + (size_t)i * D + j);
       cp_async<4>(af + (sw ? 0 : 1), beta + (size_t)i * D + j);
-      cp_async<8>(&SQ[i * RS + j], carry + (size_t)c * DD + (size_t)i * D + j);
+      cp_async<8>(&SQ[SM::e(i, j)], carry + (size_t)c * DD + (size_t)i * D + j);
     } else {
       *a = ab_pack<DP>(i, 0.0f, 1.0f);
-      SQ[i * RS + j] = make_float2(0.0f, 0.0f);
+      SQ[SM::e(i, j)] = make_float2(0.0f, 0.0f);
     }
-    Gs[i * DP + j] = make_float2(0.0f, 0.0f);
+    Gs[SM::ge(i, j)] = make_float2(0.0f, 0.0f);
   }
   cp_async_wait_all();
-  A[DP * RS + j] = ab_pack<DP>(DP, j == 0 ? 1.0f : 0.0f, 0.0f);
-  A[j * RS + DP] = make_float2(0.0f, 0.0f);
-  SQ[DP * RS + j] = make_float2(j == 0 ? 1.0f : 0.0f, 0.0f);
-  SQ[j * RS + DP] = make_float2(0.0f, 0.0f);
+  A[SM::e(DP, j)] = ab_pack<DP>(DP, j == 0 ? 1.0f : 0.0f, 0.0f);
+  SQ[SM::e(DP, j)] = make_float2(j == 0 ? 1.0f : 0.0f, 0.0f);
+  if constexpr (!SM::SW) {   // the swizzled layout has no null column (eval.cuh Smem)
+    A[SM::e(j, DP)] = make_float2(0.0f, 0.0f);
+    SQ[SM::e(j, DP)] = make_float2(0.0f, 0.0f);
+  }
   const float th = (live && j < D) ? theta[j] : 0.0f;
   __syncwarp();
   const int n = live ? (int)(cstart[c + 1] - cstart[c]) : 0;
@@ -606,7 +607,7 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
   // last chunk (their loads were clamped to chunk 0's events) are skipped.  Scratch for g_theta
   // and the lsum: the group's parameter array A (no longer read).
   float* scf = reinterpret_cast<float*>(A);
-  double* scd = reinterpret_cast<double*>(A + DP);
+  double* scd = reinterpret_cast<double*>(A + SM::e(1, 0));
   scf[j] = gth;
   if (j == 0) scd[0] = lsum;
   __syncthreads();
@@ -617,17 +618,17 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
     const int nq = (int)min((int64_t)NG, C - (int64_t)blockIdx.x * NG);
     for (int q = 0; q < nq; q++) {
       const float2* gb = reinterpret_cast<const float2*>(smem + (q / SM::G) * SM::per_warp) +
-                         (q % SM::G) * SM::per_group;
+                         SM::group_off(q % SM::G);
       if (e < (int)(2 * DD)) {
         if (grad) {
           const int pr = e >> 1;
-          const float2 v = gb[2 * SM::AS + (pr / D) * DP + (pr % D)];
+          const float2 v = gb[2 * SM::AS + SM::ge(pr / D, pr % D)];
           acc += (double)((e & 1) ? v.y : v.x);
         }
       } else if (e < (int)(2 * DD) + D) {
         if (grad) acc += (double)reinterpret_cast<const float*>(gb)[e - (int)(2 * DD)];
       } else {
-        acc += *reinterpret_cast<const double*>(gb + DP);
+        acc += *reinterpret_cast<const double*>(gb + SM::e(1, 0));
       }
     }
     rpart[(size_t)blockIdx.x * NE + e] = acc;
