@@ -3,15 +3,22 @@
 // for every fitted window, as one tensor-core GEMM with a fused tanh epilogue on sm_100a.
 //
 // It is a dense contraction: X[W][K] x Wt[K][H] with K = 2 D^2 + D, the X row of window w being
-// [alpha_w (D^2) | -beta_w T_w (D^2) | theta_w (D)] and the weight row of hidden unit h
+// [alpha_w (D^2) | beta_w (D^2) | theta_w (D)] and the weight row of hidden unit h
 // [A_h | B_h | C_h].  tcgen05.mma kind::tf32, M = 128 windows per CTA, N = H (<= 256 per CTA,
-// more as extra grid columns), K staged in chunks of 32 through a 2-deep shared-memory ring
-// (operands prefetched two chunks ahead in registers, 8 warps per CTA);
-// the fp32 accumulator lives in TMEM (128 lanes x N columns) and the epilogue reads it back with
-// tcgen05.ld, applies tanh and stores hks.  The operands are staged by the CTA's threads (not
-// TMA) because X is assembled on the fly from three parameter arrays with the per-window
-// -T_w scaling folded in; inputs are rounded to TF32 with cvt.rna (R22: error
-// <= 2^-10 of sum_k |W_hk X_wk| before tanh).
+// more as extra grid columns); the fp32 accumulators live in TMEM and the epilogue reads them
+// back with tcgen05.ld, combines them with -T_w, applies tanh and stores hks.  Two kernels:
+//   k_hawkes_features_tma (the fast path, D % 4 == 0 so every row stride is a multiple of 16
+//     bytes): a producer warp streams 128x32 tiles of alpha/beta/theta and Nx32 tiles of A/B/C
+//     with TMA (cp.async.bulk.tensor, SWIZZLE_128B, out-of-range rows and K-tails zero-filled)
+//     into a ring of stages; one thread issues the MMAs; alpha and theta chunks accumulate into
+//     TMEM columns [0, N), beta chunks into [N, 2N) (the per-window T cannot be folded into a
+//     shared operand), combined as acc0 - T_w acc1 in the epilogue.  Operands enter the tensor
+//     core as raw fp32 (top 19 bits used).  Measured 0.52 ms per 1,048,576 windows at D = 16,
+//     H = 128: 80% of the measured HBM bandwidth (profiles/r01_bench_feat_tma.jsonl).
+//   k_hawkes_features (D % 4 != 0, where TMA cannot address the rows): the CTA's threads stage
+//     the operands through registers (cvt.rna to TF32) into a 2-deep shared-memory ring in the
+//     canonical K-major SWIZZLE_NONE layout below, X assembled on the fly with -T_w folded in.
+// Precision: DESIGN.md R22 (error <= 2^-9 of sum_k |W_hk X_wk| before tanh).
 //
 // Shared-memory operand layout: the canonical K-major SWIZZLE_NONE UMMA layout of 8-row x
 // 16-byte core matrices; element (r, k) of a chunk at (r/8)*SBO + (k/4)*LBO + (r%8)*16 + (k%4)*4
