@@ -22,7 +22,8 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "smsp__issue_active.avg.pct_of_peak_sustained_active",
            "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
-           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"]
+           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+           "l1tex__data_pipe_lsu_wavefronts.sum", "l1tex__data_pipe_lsu_wavefronts_mem_lg.sum"]
 OUT = os.path.join(ROOT, "gpurun_out", "k_fit_metrics.csv")
 
 
@@ -82,6 +83,10 @@ def parse(path):
            "mufu_pct": vals.get("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
            "inst_executed": vals.get("smsp__inst_executed.sum"),
            "global_ld_sectors": vals.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"),
+           "lsu_wavefronts_all": vals.get("l1tex__data_pipe_lsu_wavefronts.sum"),
+           "lsu_wavefronts_global": vals.get("l1tex__data_pipe_lsu_wavefronts_mem_lg.sum"),
+           "mio_frac_incl_global": ((vals["l1tex__data_pipe_lsu_wavefronts.sum"] + shfl_per_ev * ev_eval) / (148 * cyc)
+                                    if "l1tex__data_pipe_lsu_wavefronts.sum" in vals else None),
            "command": " ".join(CMD), "metrics_csv": os.path.relpath(path, ROOT)}
     dst = os.path.join(ROOT, "profiles", "r02_k_fit_capture.json")
     json.dump(out, open(dst, "w"), indent=1)
