@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0,
                     help="--config cfg4: events per chunk (0: mdhp_seq_chunk_hint, whole waves)")
     ap.add_argument("--hidden", type=int, default=128, help="--config feat: MDHP-LSTM hidden size H")
+    ap.add_argument("--latency", action="store_true",
+                    help="mdhp_fit latency mode (D <= 8): one window per warp in time chunks")
     ap.add_argument("--shard-seq", action="store_true",
                     help="cfg4: split ONE sequence over the ranks (f1, strong scaling, NCCL map exchange)")
     return ap.parse_args()
@@ -258,12 +260,14 @@ def bench_seq_sharded(args, rc, world, rank, dev):
     return 0
 
 
-def fit_cfg_for(M, name, iters, tol):
+def fit_cfg_for(M, name, iters, tol, latency=False):
     """The fit each config is quoted on: cfg1 500 plain GD iterations on the mean loss (SURVEY
-    8(d)); the others Adam lr 0.05, fixed iterations or converged mode."""
+    8(d)), single-window latency in latency mode; the others Adam lr 0.05, fixed
+    iterations or converged mode."""
     if name == "cfg1":
-        return M.FitConfig(max_iters=iters, optimizer="gd", lr=0.5, loss="mean", tol_rel=tol, patience=10)
-    return M.FitConfig(max_iters=iters, optimizer="adam", lr=0.05, tol_rel=tol, patience=10)
+        return M.FitConfig(max_iters=iters, optimizer="gd", lr=0.5, loss="mean", tol_rel=tol, patience=10,
+                           latency_mode=latency)
+    return M.FitConfig(max_iters=iters, optimizer="adam", lr=0.05, tol_rel=tol, patience=10, latency_mode=latency)
 
 
 def gen_batch(rc, name, W, seed, first, dev):
@@ -656,20 +660,23 @@ def sub_results(M, args, dev):
     per-config numbers are quoted, with its roofline fraction and lnL parity."""
     from synth import gen
     subs = {}
-    plan = [("cfg1", 1, 500, 0.0, 5, 3), ("cfg2", 4096, 500, 0.0, 3, 2), ("cfg3", 65536, 500, 0.0, 1, 1)]
-    for name, W, iters, tol, steps, warm in plan:
+    plan = [("cfg1", 1, 500, 0.0, 5, 3, True), ("cfg2", 4096, 500, 0.0, 3, 2, False),
+            ("cfg3", 65536, 500, 0.0, 1, 1, False)]
+    for name, W, iters, tol, steps, warm, lat in plan:
         rc = gen.CONFIGS[name]
-        cfg = fit_cfg_for(M, name, iters, tol)
+        cfg = fit_cfg_for(M, name, iters, tol, lat)
         r = run_windows(M, rc, name, W, cfg, 1, 0, dev, steps, warm, True, args.seed, keep=True)
         d = r["data"]
         sub = {"workload": f"{name}: {W} windows, D={rc.D}, ~{r['local_E'] // max(W, 1)} events/window, T={rc.T}s, "
                            + ("plain GD lr 0.5 on the mean loss" if name == "cfg1" else "Adam lr 0.05")
-                           + f", {iters} fixed iterations + final eval",
+                           + f", {iters} fixed iterations + final eval"
+                           + (", latency mode (one window per warp in 16 time chunks)" if lat else ""),
                "value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
                "windows_fitted_per_s": r["windows_fitted_per_s"], "fit_ms": r["fit_ms"],
                "roofline": roofline_of(rc.D, r["local_ev_eval"], r["fit_ms"], "k_fit")}
         if name == "cfg1":
             sub["latency_ms_per_window_fit"] = r["fit_ms"]
+            sub["us_per_iteration"] = 1e3 * r["fit_ms"] / (iters + 1)
         if not args.no_cpu:
             sub["parity"] = oracle_lnl_parity(rc.D, d, strided(W, 4096 if name != "cfg3" else 1024))
         subs[name] = sub
@@ -759,7 +766,7 @@ def main():
         return bench_loglik(args, rc, b, W, world, rank, dev)
 
     strong = not args.weak
-    cfg = fit_cfg_for(M, args.config, args.iters, args.tol)
+    cfg = fit_cfg_for(M, args.config, args.iters, args.tol, args.latency)
     clocks = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
                           int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
     res = run_windows(M, rc, args.config, W, cfg, world, rank, dev, args.steps, args.warmup, strong,

@@ -244,6 +244,7 @@ struct FitCfgDev {
   float lr, b1, b2, eps, tol_rel, min_param;
   unsigned fit_mask;
   int step0;   // Adam steps of earlier calls (resume)
+  int latency; // latency mode (k_fit_tc): one window per warp in time chunks
 };
 
 // launch counter (process-wide), incremented by every launch site

@@ -272,18 +272,26 @@ __device__ __forceinline__ void sts2o(uint32_t a, float x, float y) {
 // contiguously (SQ = A + AS, Gs = A + 2 AS; Smem<DP>).  PRE: A holds beta' = -beta log2(e)
 // (the fit and loglik kernels) instead of beta (the sequence path), so every exponential is
 // ex2(beta' * dt) without the extra multiply.
-template <int DP, bool GRAD, bool PRE>
+template <int DP, bool GRAD, bool PRE, bool TC = false>
 __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __restrict__ A,
                                               float2* __restrict__ SQ, float2* __restrict__ Gs,
                                               const int j, const int gbase, const float th,
-                                              float& last, float& gth, double& lsum) {
+                                              float& last, float& gth, double& lsum,
+                                              const float tb = 0.0f) {
   using SM = Smem<DP>;
   constexpr bool SW = SM::SW;
   constexpr int RS = SM::RS;
   constexpr int LG = Log2<DP>::v;
   constexpr int kSQ = SM::AS * 8, kG = 2 * SM::AS * 8;   // byte offsets from A
   MDHP_ASSERT(SQ == A + SM::AS && Gs == A + 2 * SM::AS);
-  const uint32_t sA = static_cast<uint32_t>(__cvta_generic_to_shared(A));
+  uint32_t sA = static_cast<uint32_t>(__cvta_generic_to_shared(A));
+  // The parameter loads (lda*) are non-volatile asm so that ptxas may move them across the
+  // state stores inside the chunk; every address derives from sA, which this empty volatile
+  // asm (a compiler memory barrier) redefines here, so no parameter load is hoisted above the
+  // start of the chunk -- i.e. above the parameter writes of the fit (opt_action,
+  // load_window).  (Without it a loop-invariant address, e.g. Dp = 1, let the compiler hoist
+  // the load out of the fit loop.)
+  asm volatile("" : "+r"(sA) :: "memory");
   // per-lane bases.  Odd stride: row i of column j at rowb + i*RS*8, column i of row j at
   // colb + i*8, gradient row i of column j at rowb + kG + i*DP*8.  SW: element (r, c) at
   // sA + 128 r + 8 x with x = (c ^ r) & (DP-1); the row read (i, j) and the column access
@@ -298,8 +306,12 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
   for (int s = 0; s < 8; s++) {
     const float t = s == 0 ? ck.ta.x : s == 1 ? ck.ta.y : s == 2 ? ck.ta.z : s == 3 ? ck.ta.w
                   : s == 4 ? ck.tb.x : s == 5 ? ck.tb.y : s == 6 ? ck.tb.z : ck.tb.w;
-    const float dc = s == 0 ? ck.da.x : s == 1 ? ck.da.y : s == 2 ? ck.da.z : s == 3 ? ck.da.w
-                   : s == 4 ? ck.db.x : s == 5 ? ck.db.y : s == 6 ? ck.db.z : ck.db.w;
+    float dc = s == 0 ? ck.da.x : s == 1 ? ck.da.y : s == 2 ? ck.da.z : s == 3 ? ck.da.w
+             : s == 4 ? ck.db.x : s == 5 ? ck.db.y : s == 6 ? ck.db.z : ck.db.w;
+    // TC (a time chunk of a window whose carried-in state is anchored at the chunk base tb):
+    // the first event of a mark in the chunk re-anchors from tb, not from the mark's previous
+    // event (gap = t - tb, the smaller of the two; fp32 subtraction is monotone)
+    if constexpr (TC) dc = fminf(dc, t - tb);
     const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
     const int i = (int)__byte_perm(word, 0u, 0x4440u | (unsigned)(s & 3));   // mark (null: DP)
     MDHP_ASSERT(i >= 0 && i <= DP);
@@ -403,7 +415,7 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
 
 // The event loop of one window-evaluation, two chunks per iteration with explicit buffers so
 // the prefetch of chunk c+1 overlaps chunk c without register rotation.
-template <int DP, bool GRAD, bool PRE>
+template <int DP, bool GRAD, bool PRE, bool TC = false>
 __device__ __forceinline__ void event_loop(const float2* __restrict__ A, float2* __restrict__ SQ,
                                            float2* __restrict__ Gs,
                                            const int j, const int gbase,
@@ -412,28 +424,85 @@ __device__ __forceinline__ void event_loop(const float2* __restrict__ A, float2*
                                            const uint8_t* __restrict__ mk, const int64_t beg,
                                            const int n, const int nmax, const float th,
                                            float& last, float& gth, double& lsum,
-                                           const float last0 = -1.0f) {
+                                           const float last0 = -1.0f, const int clampo = -1,
+                                           const float tb = 0.0f) {
   // last0: anchor of the initial state (-1: empty history; 0: a carried-in state anchored at
-  // the chunk base, seq.cu)
+  // the chunk base, seq.cu; tb: a time chunk of a window, TC)
   last = last0;
   gth = 0.0f;
   lsum = 0.0;
-  // window base pointers; chunk offsets are clamped to the window's null chunk at npad
+  // window base pointers; chunk offsets are clamped to the window's null chunk at npad (a time
+  // chunk of a window passes the offset of its window's null chunk, clampo)
   const float* tw = t32 + beg;
   const float* dw = dtp + beg;
   const uint8_t* mw = mk + beg;
-  const int npad = (n + 7) & ~7;
+  const int npadn = (n + 7) & ~7;
+  const int npad = clampo >= 0 ? clampo : npadn;
   MDHP_ASSERT(n >= 0 && nmax >= n);
+  // offsets at or past this window's (chunk's) padded end go to the null chunk
+  auto co = [&](int off) { return off < npadn ? off : npad; };
   Chunk c0, c1;
-  load_chunk(c0, tw, dw, mw, 0 < n ? 0 : npad);
+  load_chunk(c0, tw, dw, mw, co(0));
   for (int base = 0; base < nmax; base += 16) {
-    load_chunk(c1, tw, dw, mw, min(base + 8, npad));
-    process_chunk<DP, GRAD, PRE>(c0, A, SQ, Gs, j, gbase, th, last, gth, lsum);
+    load_chunk(c1, tw, dw, mw, co(base + 8));
+    process_chunk<DP, GRAD, PRE, TC>(c0, A, SQ, Gs, j, gbase, th, last, gth, lsum, tb);
     // no early exit: a second chunk past nmax is all null events (exact no-ops), and one basic
     // block per iteration lets ptxas overlap chunk c's reduction with chunk c+1's row reads
-    load_chunk(c0, tw, dw, mw, min(base + 16, npad));
-    process_chunk<DP, GRAD, PRE>(c1, A, SQ, Gs, j, gbase, th, last, gth, lsum);
+    load_chunk(c0, tw, dw, mw, co(base + 16));
+    process_chunk<DP, GRAD, PRE, TC>(c1, A, SQ, Gs, j, gbase, th, last, gth, lsum, tb);
   }
+}
+
+// The column-update recurrence alone (phase 1 of a time-chunked window, k_fit_tc): from the
+// state in SQ (zero), every event of the chunk re-anchors its column; returns via `last` the
+// time of the latest event of source j (last0 if none).  Loads as event_loop (clampo, tb).
+template <int DP, bool PRE>
+__device__ __forceinline__ void local_loop(const float2* __restrict__ A, float2* __restrict__ SQ,
+                                           const int j, const float* __restrict__ t32,
+                                           const float* __restrict__ dtp,
+                                           const uint8_t* __restrict__ mk, const int64_t beg,
+                                           const int n, const int nmax, float& last,
+                                           const float last0, const int clampo, const float tb) {
+  using SM = Smem<DP>;
+  constexpr bool SW = SM::SW;
+  constexpr int kSQ = SM::AS * 8;
+  last = last0;
+  uint32_t sA = static_cast<uint32_t>(__cvta_generic_to_shared(A));
+  asm volatile("" : "+r"(sA) :: "memory");   // see process_chunk
+  const uint32_t colb = SW ? sA + 128u * j : sA + 8u * SM::RS * j;
+  const uint32_t colbb = colb + (ab_swapped<DP>(j) ? 0u : 4u);
+  const float* tw = t32 + beg;
+  const float* dw = dtp + beg;
+  const uint8_t* mw = mk + beg;
+  auto run8 = [&](const Chunk& ck) {
+#pragma unroll
+    for (int s = 0; s < 8; s++) {
+      const float t = s == 0 ? ck.ta.x : s == 1 ? ck.ta.y : s == 2 ? ck.ta.z : s == 3 ? ck.ta.w
+                    : s == 4 ? ck.tb.x : s == 5 ? ck.tb.y : s == 6 ? ck.tb.z : ck.tb.w;
+      float dc = s == 0 ? ck.da.x : s == 1 ? ck.da.y : s == 2 ? ck.da.z : s == 3 ? ck.da.w
+               : s == 4 ? ck.db.x : s == 5 ? ck.db.y : s == 6 ? ck.db.z : ck.db.w;
+      dc = fminf(dc, t - tb);
+      const int i = (int)__byte_perm(s < 4 ? ck.mm.x : ck.mm.y, 0u, 0x4440u | (unsigned)(s & 3));
+      MDHP_ASSERT(i >= 0 && i <= DP);
+      const uint32_t x = SW ? (((uint32_t)(i ^ j) & (uint32_t)(DP - 1)) << 3) : ((uint32_t)i << 3);
+      const float bc = lda1o<0>(colbb + x);
+      const float2 sc = lds2o<kSQ>(colb + x);
+      const float ec = PRE ? ex2f(bc * dc) : ex2f(bc * (dc * -kLog2e));
+      if (!SW || i < DP) sts2o<kSQ>(colb + x, fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
+      last = fsel_eqi(i, j, t, last);
+    }
+  };
+  const int npadn = (n + 7) & ~7;
+  auto co = [&](int off) { return off < npadn ? off : clampo; };
+  Chunk c0, c1;
+  load_chunk(c0, tw, dw, mw, co(0));
+  for (int base = 0; base < nmax; base += 16) {
+    load_chunk(c1, tw, dw, mw, co(base + 8));
+    run8(c0);
+    load_chunk(c0, tw, dw, mw, co(base + 16));
+    run8(c1);
+  }
+  __syncwarp();
 }
 
 // Per-lane epilogue data of source column j.

@@ -629,6 +629,256 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
   tm_free(tbase, TL::ALLOC);
 }
 
+// ---------------------------------------------------------------- latency mode (time chunks)
+// mdhp_fit_config.latency_mode, Dp <= 8: ONE window per warp, its events cut into G = 32/Dp
+// consecutive time chunks (boundaries on 8-event blocks, never inside a tie group), one per
+// group of Dp lanes, so a window's sequential event chain is ~G times shorter (single windows
+// and small batches, BASELINE cfg1).  Per evaluation (the a7 chunked scan inside a warp):
+//   phase 1: every group runs its chunk's column updates from a zero state (local_loop) and
+//            re-anchors the local state at the chunk's last event t_e;
+//   scan:    the affine maps of the chunks (decay over the chunk span + local state,
+//            seq.cu AffMap) are scanned across the groups with warp shuffles; the state
+//            carried into chunk g is the composite of chunks 0..g-1, anchored at the chunk
+//            base t_b (the previous chunk's last event);
+//   phase 3: every group runs the full event loop of its chunk from the carried state;
+//   then the groups' gradient accumulators, sum ln lambda and sum 1/lambda are added in a fixed
+//   order (identical in every group) and every group finishes the epilogue from the last
+//   chunk's final state, so all groups hold the same lnL, gradients and (after opt_action)
+//   parameters.  Results equal the plain kernel's within fp32 rounding (a different but fixed
+//   summation order), deterministic run to run.
+struct TcChunk {
+  int b, n;           // first event (relative to the window) and count of this group's chunk
+  int clampo;         // offset of the window's null chunk, relative to b
+  float tb, te;       // chunk base (last event before it, -1 if none) and last event time
+};
+
+template <int DP>
+__device__ __forceinline__ TcChunk tc_chunk(const Packed& P, int64_t beg, int n, int g) {
+  constexpr int G = 32 / DP;
+  // boundaries b_0 = 0 <= b_1 <= ... <= b_G = n: near k n / G, on 8-event blocks, moved past
+  // cross-mark tie groups (a chunk must not start at a time equal to its base)
+  int lo = 0, hi = n;
+  int prev = 0;
+  for (int k = 1; k <= g + 1 && k <= G; k++) {
+    int b = k == G ? n : (int)(((int64_t)n * k / G) & ~(int64_t)7);
+    if (b < prev) b = prev;
+    while (b > 0 && b < n && P.t32[beg + b] == P.t32[beg + b - 1]) b = min(b + 8, n);
+    if (k == g) lo = b;
+    if (k == g + 1) hi = b;
+    prev = b;
+  }
+  TcChunk ch;
+  ch.b = lo;
+  ch.n = hi - lo;
+  ch.clampo = ((n + 7) & ~7) - lo;
+  ch.tb = lo > 0 ? P.t32[beg + lo - 1] : -1.0f;
+  ch.te = hi > 0 ? P.t32[beg + hi - 1] : -1.0f;
+  return ch;
+}
+
+struct TcMap {
+  float E, L, Sb, Qb;   // decay over the span, span, state added (S, Q') -- seq.cu AffMap
+};
+__device__ __forceinline__ TcMap tc_compose(const TcMap& m1, const TcMap& m2) {
+  TcMap r;
+  r.E = m2.E * m1.E;
+  r.L = m1.L + m2.L;
+  r.Sb = fmaf(m2.E, m1.Sb, m2.Sb);
+  r.Qb = fmaf(m2.E, fmaf(m2.L, m1.Sb, m1.Qb), m2.Qb);
+  return r;
+}
+
+template <int DP, bool GRAD>
+__device__ __forceinline__ double eval_window_tc(const Packed& P, float2* A, float2* SQ,
+                                                 float2* Gs, float2* wbase, const WarpCtx<DP>& c,
+                                                 int64_t w, bool live, const TcChunk& ch,
+                                                 float th, const ColInfo& ci, float& dth,
+                                                 bool& finite, bool& exact) {
+  using SM = Smem<DP>;
+  constexpr int G = SM::G;
+  const int64_t beg = live ? P.begin[w] : 0;
+  const int n = live ? ch.n : 0;
+  const int nmax = group_max_i<DP>(n);
+  // ---- phase 1: the chunk's column updates from a zero state
+  reset_state<DP>(SQ, Gs, c.j);
+  __syncwarp();
+  float lastl;
+  local_loop<DP, true>(A, SQ, c.j, P.t32, P.dtp, P.mark, beg + ch.b, n, nmax, lastl, ch.tb,
+                       ch.clampo, ch.tb);
+  // ---- local state at the chunk end (anchor te), as this chunk's affine map per pair (r, j)
+  TcMap m[DP];
+  const float L = ch.te - ch.tb;
+  const float dl = ch.te - lastl;
+#pragma unroll
+  for (int r = 0; r < DP; r++) {
+    const float2 k = A[SM::e(r, c.j)];
+    const float b = ab_beta<DP>(r, k);   // beta' (A holds -beta log2 e)
+    const float2 sq = SQ[SM::e(r, c.j)];
+    const float e = ex2f(b * dl);
+    m[r].E = ex2f(b * L);
+    m[r].L = L;
+    m[r].Sb = e * sq.x;
+    m[r].Qb = e * fmaf(dl, sq.x, sq.y);
+  }
+  // ---- inclusive scan of the maps over the groups (lane j of group g <- lane j of g - k)
+#pragma unroll
+  for (int k = 1; k < G; k <<= 1) {
+#pragma unroll
+    for (int r = 0; r < DP; r++) {
+      TcMap up;
+      up.E = __shfl_up_sync(kFull, m[r].E, k * DP);
+      up.L = __shfl_up_sync(kFull, m[r].L, k * DP);
+      up.Sb = __shfl_up_sync(kFull, m[r].Sb, k * DP);
+      up.Qb = __shfl_up_sync(kFull, m[r].Qb, k * DP);
+      if (c.g >= k) m[r] = tc_compose(up, m[r]);
+    }
+  }
+  // ---- phase 3: the full event loop of the chunk from the carried state (the composite of
+  // the earlier chunks applied to the empty initial state), anchored at tb
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < DP; r++) {
+    const float cs = __shfl_up_sync(kFull, m[r].Sb, DP);
+    const float cq = __shfl_up_sync(kFull, m[r].Qb, DP);
+    SQ[SM::e(r, c.j)] = c.g > 0 ? make_float2(cs, cq) : make_float2(0.0f, 0.0f);
+    Gs[SM::ge(r, c.j)] = make_float2(0.0f, 0.0f);
+  }
+  __syncwarp();
+  float last, gth;
+  double lsum;
+  event_loop<DP, GRAD, true, true>(A, SQ, Gs, c.j, c.gbase, P.t32, P.dtp, P.mark, beg + ch.b, n,
+                                   nmax, th, last, gth, lsum, ch.b > 0 ? ch.tb : -1.0f,
+                                   ch.clampo, ch.tb);
+  // ---- sums over the chunks, in the same order in every group
+#pragma unroll
+  for (int o = DP; o < 32; o <<= 1) gth += __shfl_xor_sync(kFull, gth, o);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) lsum += __shfl_xor_sync(kFull, lsum, o);
+  __syncwarp();
+  float2 gtot[DP];
+  if (GRAD) {
+#pragma unroll
+    for (int r = 0; r < DP; r++) {
+      float2 a = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int q = 0; q < G; q++) {
+        const float2 v = (wbase + SM::group_off(q) + 2 * SM::AS)[SM::ge(r, c.j)];
+        a.x += v.x;
+        a.y += v.y;
+      }
+      gtot[r] = a;
+    }
+  }
+  // ---- epilogue from the last chunk's final state (its SQ and its lanes' last times)
+  const float2* SQl = wbase + SM::group_off(G - 1) + SM::AS;
+  ColInfo cc = ci;
+  cc.last = __shfl_sync(kFull, last, (G - 1) * DP + c.j);
+  Series S;
+  load_series(S, P.mom + ((size_t)(live ? w : 0) * P.Dp + c.j) * kMom, live && cc.N > 0);
+  double part3 = 0.0;
+  bool ok = true;
+  float2 gout[DP];
+#pragma unroll 4
+  for (int i = 0; i < DP; i++) {
+    const float2 k = A[SM::e(i, c.j)];
+    const float2 sq = SQl[SM::e(i, c.j)];
+    float Eb, Hb2;
+    const float ka = ab_alpha<DP>(i, k), kb = ab_beta<DP>(i, k) * -kLn2;
+    compensator(cc, S, kb, sq.x, sq.y, Eb, Hb2);
+    gout[i] = make_float2(0.0f, 0.0f);
+    if (cc.real && i < P.D) {
+      part3 += (double)(ka * Eb);
+      if (GRAD) {
+        const float da = gtot[i].x + Eb;
+        const float db = fmaf(-ka, gtot[i].y, ka * Hb2);
+        ok = ok && isfinite(da) && isfinite(db);
+        gout[i] = make_float2(da, db);
+      }
+    }
+  }
+  __syncwarp();   // every group has read the others' accumulators
+  if (GRAD) {
+#pragma unroll
+    for (int i = 0; i < DP; i++) Gs[SM::ge(i, c.j)] = gout[i];
+  }
+  dth = gth - ci.T;
+  if (GRAD && cc.real) ok = ok && isfinite(dth);
+  part3 = group_sum_d<DP>(part3);
+  const double sth = group_sum_d<DP>(cc.real ? (double)th : 0.0);
+  const double lnl = (double)kLn2 * lsum + part3 - (double)ci.T * sth;
+  finite = __all_sync(kFull, ok) && isfinite(lnl);
+  const int ntot = live ? P.n[w] : 0;
+  exact = live && needs_exact(lnl, ntot, (double)kLn2 * lsum, (double)ci.T * sth, part3);
+  __syncwarp();
+  return lnl;
+}
+
+template <int DP, bool RESUME>
+__global__ void __launch_bounds__(128, 4)
+k_fit_tc(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ alpha,
+         float* __restrict__ beta, float* __restrict__ opt, double* __restrict__ lnl_out,
+         int32_t* __restrict__ iters_out, int32_t* __restrict__ status,
+         float* __restrict__ trace, int* __restrict__ counter, int32_t* __restrict__ xlist,
+         int32_t* __restrict__ xcount) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using SM = Smem<DP>;
+  using TL = TmCols<DP>;
+  static_assert(DP <= 8, "latency mode: Dp <= 8");
+  WarpCtx<DP> c;
+  const int wid = threadIdx.x >> 5;
+  float2* wbase = reinterpret_cast<float2*>(smem + wid * SM::per_warp);
+  float2* A = wbase + SM::group_off(c.g);
+  float2* SQ = A + SM::AS;
+  float2* Gs = A + 2 * SM::AS;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + (blockDim.x >> 5) * SM::per_warp);
+  const uint32_t tbase = tm_alloc(slot, TL::ALLOC);
+  const uint32_t tm = tbase + ((uint32_t)((wid & 3) * 32) << 16);
+  const int D = P.D;
+  for (;;) {
+    int64_t unit = 0;
+    if (c.lane == 0) unit = atomicAdd(counter, 1);
+    unit = __shfl_sync(kFull, unit, 0);
+    if (unit >= P.W) break;
+    const int64_t w = P.perm[unit];
+    MDHP_ASSERT(w >= 0 && w < P.W);
+    const int st0 = status[w];
+    const bool live = !(st0 & MDHP_ST_INVALID);
+    float th = load_window<DP>(A, c, D, w, true, live, tm, 0.0f, theta, alpha, beta, opt);
+    const ColInfo ci = col_info<DP>(P, w, live, c.j);
+    const int n = live ? P.n[w] : 0;
+    const TcChunk ch = tc_chunk<DP>(P, live ? P.begin[w] : 0, n, c.g);
+    const float scale = (cfg.loss_mean && n > 0) ? 1.0f / (float)n : 1.0f;
+    WinCtl ctl;
+    ctl.lr_w = cfg.lr;
+    bool done = !live || cfg.max_iters <= 0;
+    while (!done) {   // one window per warp: warp-uniform
+      float dth;
+      bool finite, exact;
+      const double lnl = eval_window_tc<DP, true>(P, A, SQ, Gs, wbase, c, w, live, ch, th, ci, dth,
+                                                  finite, exact);
+      const int act = ctl.decide(cfg, lnl, finite, done, trace, w, c.lane == 0);
+      if (act != ACT_NONE)
+        opt_action<DP, RESUME>(A, Gs, c, D, cfg, act, ctl.lr_w, ctl.s, scale, dth, th, tm);
+      __syncwarp();
+    }
+    float dth;
+    bool finite, exact;
+    const double lnl = eval_window_tc<DP, false>(P, A, SQ, Gs, wbase, c, w, live, ch, th, ci, dth,
+                                                 finite, exact);
+    store_window<DP>(A, c, D, w, live && c.g == 0, th, tm, theta, alpha, beta, opt);
+    if (c.lane == 0) {
+      lnl_out[w] = live ? lnl : (double)NAN;
+      iters_out[w] = ctl.it;
+      status[w] = (st0 & kKeepStatus) | ctl.st;
+      if (exact) list_exact(xlist, xcount, w);
+      if (trace && live)
+        for (int q = ctl.it; q < cfg.max_iters; q++) trace[(size_t)w * cfg.max_iters + q] = NAN;
+    }
+    __syncwarp();
+  }
+  tm_free(tbase, TL::ALLOC);
+}
+
 // ---------------------------------------------------------------- host launchers
 template <int DP>
 static int launch_loglik_t(const Packed& P, const float* th, const float* al, const float* be,
@@ -676,6 +926,14 @@ static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float*
   // converged mode (tol_rel > 0): windows stop at different iterations -> per-window refill
   auto kern = cfg.tol_rel > 0.0f ? (cfg.step0 != 0 ? k_fit<DP, true, true> : k_fit<DP, false, true>)
                                  : (cfg.step0 != 0 ? k_fit<DP, true, false> : k_fit<DP, false, false>);
+  // latency mode (Dp <= 8): one window per warp, its events in 32/Dp time chunks (k_fit_tc)
+  bool tc = false;
+  if constexpr (DP <= 8) {
+    if (cfg.latency) {
+      kern = cfg.step0 != 0 ? k_fit_tc<DP, true> : k_fit_tc<DP, false>;
+      tc = true;
+    }
+  }
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess) {
     set_error("cudaFuncSetAttribute(k_fit) failed");
@@ -706,7 +964,7 @@ static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float*
     fprintf(stderr, "k_fit<%d>: per_sm=%d (regs %d smem %d tmem %d) smem=%zu regs=%d local=%zu\n", DP,
             per_sm, by_regs, by_smem, by_tmem, smem, fa.numRegs, fa.localSizeBytes);
   if (per_sm < 1) per_sm = 1;
-  const int64_t units = (P.W + SM::G - 1) / SM::G;
+  const int64_t units = tc ? P.W : (P.W + SM::G - 1) / SM::G;
   int64_t blocks = (int64_t)sms * per_sm;
   const int64_t need = (units + WPB - 1) / WPB;
   if (blocks > need) blocks = need;

@@ -125,9 +125,11 @@ def test_cfg5_full():
     _run("cfg5", 1 << 20, 16, 64, 128, 3)
 
 
-def test_cfg1_500_gd():
+@pytest.mark.parametrize("latency", [False, True])
+def test_cfg1_500_gd(latency):
     """Config 1: one window, D = 2, ~200 events, T = 10 s, 500 GD iterations (mean loss) from
-    the SPEC init: fitted parameters within 1e-3 of the oracle's."""
+    the SPEC init: fitted parameters within 1e-3 of the oracle's (throughput layout and latency
+    mode, the one bench.py times for cfg1)."""
     D = 2
     b = gen.make_batch(gen.CONFIGS["cfg1"], 1, seed=2024, params=gen.CFG1_PARAMS)
     t, m = b["t"], b["mark"]
@@ -138,7 +140,7 @@ def test_cfg1_500_gd():
     kw = dict(max_iters=500, optimizer="gd", lr=0.5, loss="mean", tol_rel=0.0)
     th = torch.full((1, D), 0.1, device=DEV); al = torch.full((1, D, D), 0.5, device=DEV)
     be = torch.full((1, D, D), 1.0, device=DEV)
-    fr = M.fit(pk, th, al, be, M.FitConfig(**kw), trace=True)
+    fr = M.fit(pk, th, al, be, M.FitConfig(latency_mode=latency, **kw), trace=True)
     torch.cuda.synchronize()
     t32, T32, st = oracle.convert_window(D, t, m, 10.0, tie_policy=oracle.TIE_NUDGE)
     o = oracle.fit(D, t32, m, T32, [0.1, 0.1], np.full((2, 2), 0.5), np.ones((2, 2)), oracle.FitConfig(**kw),

@@ -506,3 +506,71 @@ def test_wrappers_reject_mismatched_sizes():
     with pytest.raises(ValueError):
         M.fit_host(D, t.cpu(), m.cpu(), off.cpu(), T.cpu(), th.cpu()[:-1].contiguous(), al.cpu(), be.cpu(),
                    M.FitConfig(max_iters=1))
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("opt", ["gd", "adam"])
+def test_fit_latency_mode_vs_oracle(D, opt):
+    """Latency mode (one window per warp, its events in 32/Dp time chunks scanned inside the
+    warp; mdhp_fit_config.latency_mode): fitted parameters within R17 and lnL within 1e-4 of
+    the oracle's fit, on recipe windows plus the edge windows (empty, tiny, ties, events at 0
+    and T) -- chunks shorter than 8 events, empty chunks and tie groups at chunk boundaries."""
+    b, _ = H.small_batch(D, 10, seed=900 + D, edges=True)
+    W = len(b["T"])
+    rng = np.random.default_rng(D)
+    th0 = rng.uniform(0.5, 5.0, (W, D)); al0 = rng.uniform(0.0, 3.0, (W, D, D)); be0 = rng.uniform(2.0, 40.0, (W, D, D))
+    kw = dict(max_iters=25, optimizer=opt, lr=0.02 if opt == "adam" else 0.05, loss="mean" if opt == "gd" else "sum",
+              tol_rel=0.0)
+    pk = M.pack_windows(D, *dev_batch(b))
+    tt = [torch.tensor(f32(x), device=DEV) for x in (th0, al0, be0)]
+    r = M.fit(pk, *tt, M.FitConfig(latency_mode=True, **kw))
+    torch.cuda.synchronize()
+    t32, T32, st = H.oracle_times(b, D)
+    for w in range(W):
+        if st[w] & oracle.INVALID_MASK:
+            continue
+        a, z = b["win_off"][w], b["win_off"][w + 1]
+        o = oracle.fit(D, t32[a:z], b["mark"][a:z], T32[w], f32(th0[w]).astype(float), f32(al0[w]).astype(float),
+                       f32(be0[w]).astype(float), oracle.FitConfig(**kw))
+        assert int(r["iters"][w]) == o["iters"]
+        for got, ref in ((tt[0][w], o["theta"]), (tt[1][w], o["alpha"]), (tt[2][w], o["beta"])):
+            got = got.cpu().numpy().astype(np.float64)
+            s = 1e-2 * max(np.mean(np.abs(ref)), 1e-4)
+            assert np.all(np.abs(got - ref) <= 1e-3 * np.maximum(np.abs(ref), s)), (D, w, got, ref)
+        assert abs(float(r["lnl"][w]) - o["lnl"]) <= 1e-4 * abs(o["lnl"]), (D, w)
+
+
+def test_fit_latency_mode_long_windows_and_determinism():
+    """Latency mode on long windows with many cross-mark ties (D = 8, 4 chunks; D = 2, 16
+    chunks): lnL after 30 Adam iterations within 1e-4 of the oracle's fit, and bit-identical
+    results run to run."""
+    for D in (2, 8):
+        rng = np.random.default_rng(77 + D)
+        wins = []
+        for w in range(3):
+            n = int(rng.integers(300, 900))
+            t = np.sort(rng.uniform(0.0, 1.0, n))
+            m = rng.integers(0, D, n).astype(np.int32)
+            for k in range(1, n - 1, 9):
+                if m[k] != m[k - 1]:
+                    t[k] = t[k - 1]
+            wins.append((t, m))
+        b = H.batch_from_windows(wins, 1.0)
+        W = len(wins)
+        kw = dict(max_iters=30, optimizer="adam", lr=0.05, tol_rel=0.0)
+        pk = M.pack_windows(D, *dev_batch(b))
+        outs = []
+        for _ in range(2):
+            tt = [torch.full((W, D), 0.1, device=DEV), torch.full((W, D, D), 0.5, device=DEV),
+                  torch.full((W, D, D), 1.0, device=DEV)]
+            r = M.fit(pk, *tt, M.FitConfig(latency_mode=True, **kw))
+            torch.cuda.synchronize()
+            outs.append([x.clone() for x in tt] + [r["lnl"].clone()])
+        for x, y in zip(*outs):
+            assert torch.equal(x, y)
+        t32, T32, _ = H.oracle_times(b, D)
+        for w in range(W):
+            a, z = b["win_off"][w], b["win_off"][w + 1]
+            o = oracle.fit(D, t32[a:z], b["mark"][a:z], T32[w], np.full(D, 0.1), np.full((D, D), 0.5),
+                           np.full((D, D), 1.0), oracle.FitConfig(**kw))
+            assert abs(float(outs[0][3][w]) - o["lnl"]) <= 1e-4 * abs(o["lnl"]), (D, w)
