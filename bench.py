@@ -797,6 +797,9 @@ def main():
                                "algorithmic count)"}
     if cap and "mio_frac" in cap:
         roof["mio"]["ncu_measured_frac"] = cap["mio_frac"]
+        if cap.get("mio_frac_incl_global") is not None:
+            # the event loads' L1 data-stage wavefronts use the same pipe (verdict r1 item 7)
+            roof["mio"]["ncu_measured_frac_incl_global_loads"] = cap["mio_frac_incl_global"]
     roof["fit_ms_avg"] = res["fit_ms"]
     roof["fit_share_of_step"] = res["fit_ms"] / res["ms_per_step"]
 

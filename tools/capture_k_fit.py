@@ -52,7 +52,10 @@ def parse(path):
         if len(r) < len(h) or "k_fit" not in r[ix["Kernel Name"]]:
             continue
         name = r[ix["Metric Name"]]
-        vals[name] = float(r[ix["Metric Value"]].replace(",", ""))
+        try:
+            vals[name] = float(r[ix["Metric Value"]].replace(",", ""))
+        except ValueError:   # "n/a": not collectable on this driver
+            continue
         units[name] = r[ix["Metric Unit"]]
         kernel = r[ix["Kernel Name"]]
     plain = json.loads(open(os.path.join(ROOT, "gpurun_out", "k_fit_capture_plain.jsonl")).read())
