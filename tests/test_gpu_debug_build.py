@@ -16,7 +16,8 @@ def test_parity_suites_under_bounds_asserts():
     lib = build.build(debug=True)
     env = dict(os.environ, MDHP_LIB=lib)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
-                        "tests/test_gpu_parity.py", "tests/test_gpu_seq.py", "tests/test_gpu_dense.py"],
+                        "tests/test_gpu_parity.py", "tests/test_gpu_seq.py", "tests/test_gpu_dense.py",
+                        "tests/test_gpu_fuzz.py", "tests/test_gpu_shard.py"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "passed" in r.stdout

@@ -156,7 +156,8 @@ def test_cfg5_full_bench_fit_500():
     """The bench step itself: 1,048,576 cfg5 windows, SPEC init, Adam lr 0.05, 500 fixed
     iterations in one persistent mdhp_fit launch; the fitted lnL of 128 strided windows (every
     8,192nd, plus the last) equals the fp64 oracle's 500-iteration fit within 1e-4 relative (R18:
-    long Adam runs are compared through lnL), and every window's lnL is finite."""
+    long Adam runs are compared through lnL), every window's lnL is finite, and the returned lnL
+    of every 4th window equals Eq.(5) at its returned parameters within 1e-4."""
     W, D = 1 << 20, 16
     b = sg.make_batch_gpu("cfg5", W, seed=2024)
     pk = M.pack_windows(D, b["t"], b["mark"], b["win_off"], b["T"], time_mode=1)
@@ -176,3 +177,27 @@ def test_cfg5_full_bench_fit_500():
     assert np.all(o["iters"] == 500)
     rel = _lnl_rel(lnl[windows], o["lnl"])
     assert np.all(rel <= 1e-4), (int(windows[np.argmax(rel)]), float(rel.max()))
+    # the returned lnL against Eq.(5) at the returned parameters, every 4th window (262,144)
+    win4 = np.arange(0, W, 4)
+    t32, m, off, T32 = _subset(b, D, win4)
+    p = [x[win4].double().cpu().numpy() for x in (th, al, be)]
+    ref = oracle.loglik_batch(D, t32, m, off, T32, *p, grads=False)
+    rel = _lnl_rel(lnl[win4], ref["lnl"])
+    assert np.all(rel <= 1e-4), (int(win4[np.argmax(rel)]), float(rel.max()))
+
+
+def test_cfg5_every_window_lnl():
+    """north_star: "fp32 log-likelihood within 1e-4 relative of the fp64 oracle on every window"
+    -- all 1,048,576 cfg5 windows (1.05e9 events) at the generating parameters, mdhp_loglik_grad
+    vs oracle.loglik_batch (lnL only) on all host cores."""
+    W = 1 << 20
+    b = sg.make_batch_gpu("cfg5", W, seed=2024)
+    D = b["D"]
+    pk = M.pack_windows(D, b["t"], b["mark"], b["win_off"], b["T"], time_mode=1)
+    r = M.loglik_grad(pk, b["theta"], b["alpha"], b["beta"], grads=False)
+    torch.cuda.synchronize()
+    t32, m, off, T32 = _subset(b, D, range(W))
+    p = [x.double().cpu().numpy() for x in (b["theta"], b["alpha"], b["beta"])]
+    ref = oracle.loglik_batch(D, t32, m, off, T32, *p, grads=False)
+    rel = _lnl_rel(r["lnl"].cpu().numpy(), ref["lnl"])
+    assert np.all(rel <= 1e-4), (int(np.argmax(rel)), float(rel.max()))
