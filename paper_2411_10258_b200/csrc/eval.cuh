@@ -362,9 +362,6 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     // no __syncwarp per event (it cost an issue slot each): the state accesses are volatile asm
     // in program order and the warp is converged, so the shared-memory unit sees one event's
     // column stores before the next event's row loads
-#ifdef MDHP_AB_EVENT_SYNCWARP
-    __syncwarp();
-#endif
   }
   __syncwarp();
   if constexpr (DP >= 8) {

@@ -325,9 +325,6 @@ __device__ __forceinline__ void opt_action(float2* A, const float2* Gs, const Wa
                                            int D, const FitCfgDev& cfg, int act, float lr_w,
                                            int s, float scale, float dth, float& th, uint32_t tm) {
   using SM = Smem<DP>;
-#ifdef MDHP_AB_NO_OPT
-  return;   // A/B timing probe only: no optimizer action
-#endif
   using L = TmCols<DP>;
   constexpr int CH = L::CH;
   const bool real = c.j < D;
