@@ -574,3 +574,42 @@ def test_fit_latency_mode_long_windows_and_determinism():
             o = oracle.fit(D, t32[a:z], b["mark"][a:z], T32[w], np.full(D, 0.1), np.full((D, D), 0.5),
                            np.full((D, D), 1.0), oracle.FitConfig(**kw))
             assert abs(float(outs[0][3][w]) - o["lnl"]) <= 1e-4 * abs(o["lnl"]), (D, w)
+
+
+def test_fit_latency_mode_converged_and_resume():
+    """Latency mode in converged mode (tol_rel, patience) matches the oracle's stop iteration,
+    status and lnL; and checkpoint/resume in latency mode equals one uninterrupted fit bit for
+    bit (adam_step0)."""
+    D = 3
+    b, _ = H.small_batch(D, 6, seed=500, edges=True)
+    W = len(b["T"])
+    th0 = np.full((W, D), 2.0); al0 = np.full((W, D, D), 10.0); be0 = np.full((W, D, D), 20.0)
+    kw = dict(max_iters=2000, optimizer="adam", lr=0.05, tol_rel=1e-6, patience=10)
+    pk = M.pack_windows(D, *dev_batch(b))
+    tt = [torch.tensor(f32(x), device=DEV) for x in (th0, al0, be0)]
+    r = M.fit(pk, *tt, M.FitConfig(latency_mode=True, **kw))
+    torch.cuda.synchronize()
+    t32, T32, st = H.oracle_times(b, D)
+    st_g = pk.status.cpu().numpy()[:W]
+    for w in range(W):
+        if st[w] & oracle.INVALID_MASK:
+            continue
+        a, z = b["win_off"][w], b["win_off"][w + 1]
+        o = oracle.fit(D, t32[a:z], b["mark"][a:z], T32[w], th0[w], al0[w], be0[w], oracle.FitConfig(**kw))
+        assert (st_g[w] & mdhp.ST_CONVERGED) == (o["status"] & oracle.CONVERGED)
+        assert abs(float(r["lnl"][w]) - o["lnl"]) <= 1e-4 * max(abs(o["lnl"]), 1.0)
+    # resume
+    P = D + 2 * D * D
+    kw2 = dict(optimizer="adam", lr=0.05, tol_rel=0.0, latency_mode=True)
+    init = [torch.tensor(f32(x), device=DEV) for x in (th0, al0, be0)]
+    a_ = [x.clone() for x in init]
+    opt_a = torch.zeros(W, 2 * P, device=DEV)
+    ra = M.fit(pk, *a_, M.FitConfig(max_iters=60, **kw2), opt_state=opt_a)
+    c_ = [x.clone() for x in init]
+    opt_c = torch.zeros(W, 2 * P, device=DEV)
+    M.fit(pk, *c_, M.FitConfig(max_iters=35, **kw2), opt_state=opt_c)
+    rc = M.fit(pk, *c_, M.FitConfig(max_iters=25, adam_step0=35, **kw2), opt_state=opt_c)
+    torch.cuda.synchronize()
+    for x, y in zip(a_, c_):
+        assert torch.equal(x, y)
+    assert torch.equal(opt_a, opt_c) and torch.equal(ra["lnl"], rc["lnl"])
