@@ -62,13 +62,16 @@ def main(n):
 
 
 
-def fit_sweep(n, iters=5):
+def fit_sweep(n, iters=5, latency=False):
     """Random-start Adam fits (lr 0.02, `iters` iterations) vs the oracle's: parameters within
-    R17 (1e-3 relative, floor 1e-2 of the group mean); prints the worst ratio to that bar."""
+    R17 (1e-3 relative, floor 1e-2 of the group mean); prints the worst ratio to that bar.
+    latency: mdhp_fit latency mode (one window per warp in time chunks; D <= 8 only)."""
     worst, windows = 0.0, 0
     for k in range(n):
         rng = np.random.default_rng(70000 + k)
         D = int(rng.integers(1, 33))
+        if latency:
+            D = 1 + (D - 1) % 8
         W = int(rng.integers(1, 16))
         b = fuzz_windows(rng, D, W)
         th, al, be = fuzz_params(rng, W, D)
@@ -79,7 +82,7 @@ def fit_sweep(n, iters=5):
                torch.tensor(b["T"], dtype=torch.float64, device="cuda"))
         pk = M.pack_windows(D, *dev)
         tt = [torch.tensor(f32(x), device="cuda") for x in (th, al, be)]
-        M.fit(pk, *tt, M.FitConfig(max_iters=iters, optimizer="adam", lr=0.02, tol_rel=0.0))
+        M.fit(pk, *tt, M.FitConfig(max_iters=iters, optimizer="adam", lr=0.02, tol_rel=0.0, latency_mode=latency))
         g = [x.cpu().numpy() for x in tt]
         t32, T32, _ = H.oracle_times(b, D)
         ocfg = oracle.FitConfig(max_iters=iters, optimizer="adam", lr=0.02, tol_rel=0.0)
@@ -95,12 +98,12 @@ def fit_sweep(n, iters=5):
                     print(f"  fit out of bar: batch {k} D={D} window {w} n={z - a} {key} ratio {r:.3g}", flush=True)
                 worst = max(worst, r)
             windows += 1
-    print(f"fit sweep: {n} batches, {windows} windows, {iters} Adam iterations: worst parameter error "
+    print(f"fit sweep{' (latency mode)' if latency else ''}: {n} batches, {windows} windows, {iters} Adam iterations: worst parameter error "
           f"{worst:.3g} x the R17 tolerance (bar 1)")
     return 0 if worst <= 1 else 1
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "fit":
-        sys.exit(fit_sweep(int(sys.argv[2]) if len(sys.argv) > 2 else 200))
+    if len(sys.argv) > 1 and sys.argv[1] in ("fit", "fit-latency"):
+        sys.exit(fit_sweep(int(sys.argv[2]) if len(sys.argv) > 2 else 200, latency=sys.argv[1] == "fit-latency"))
     sys.exit(main(int(sys.argv[1]) if len(sys.argv) > 1 else 300))
