@@ -619,16 +619,22 @@ def run_seq(M, rc, iters, steps, warmup, seed, first, dev, chunk=0, parity=False
     out = {"value": N * it / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "us_per_iteration": 1e3 * ms / (it + 1),
            "events": N, "chunk_events": ce, "iterations": it, "launches_per_step": (M.launch_count() - L0) / steps,
            "roofline": roofline_of(D, N * (it + 1), ms, "k_seq (all phases)")}
+    out["state"] = (D, rc.T, b["t"], b["mark"], th, al, be, float(r["lnl"][0]))
     if parity:
-        import oracle
-        t0 = time.perf_counter()
-        ref = oracle.loglik_rec(D, b["t"].cpu().numpy(), b["mark"].cpu().numpy(), rc.T, th.double().cpu().numpy(),
-                                al.double().cpu().numpy(), be.double().cpu().numpy(), grads=False)
-        got = float(r["lnl"][0])
-        out["parity"] = {"max_rel_lnl": abs(got - ref["lnl"]) / abs(ref["lnl"]), "n_windows_checked": 1, "bar": 1e-4,
-                         "what": "GPU lnL at the returned parameters vs the fp64 oracle (fp64 times)",
-                         "oracle_s": round(time.perf_counter() - t0, 2)}
+        out.update(run_seq_parity(out))
     return out
+
+
+def run_seq_parity(o):
+    """lnL parity of a sequence fit: the fp64 oracle on the fp64 times at the returned parameters."""
+    import oracle
+    D, T, t, m, th, al, be, got = o["state"]
+    t0 = time.perf_counter()
+    ref = oracle.loglik_rec(D, t.cpu().numpy(), m.cpu().numpy(), T, th.double().cpu().numpy(),
+                            al.double().cpu().numpy(), be.double().cpu().numpy(), grads=False)
+    return {"parity": {"max_rel_lnl": abs(got - ref["lnl"]) / abs(ref["lnl"]), "n_windows_checked": 1, "bar": 1e-4,
+                       "what": "GPU lnL at the returned parameters vs the fp64 oracle (fp64 times)",
+                       "oracle_s": round(time.perf_counter() - t0, 2)}}
 
 
 def bench_seq(args, rc, world, rank, dev):
@@ -639,6 +645,7 @@ def bench_seq(args, rc, world, rank, dev):
     if args.shard_seq:
         return bench_seq_sharded(args, rc, world, rank, dev)
     o = run_seq(M, rc, args.iters, args.steps, args.warmup, args.seed, rank, dev, chunk=args.chunk)
+    o.pop("state", None)
     if rank == 0:
         print(json.dumps({"metric": METRIC, "value": world * o["value"], "unit": UNIT, "n_gpus": world,
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": o["ms_per_step"],
@@ -655,48 +662,52 @@ def bench_seq(args, rc, world, rank, dev):
     return 0
 
 
-def sub_results(M, args, dev):
+def sub_results(M, args, dev, gpu_index):
     """N = 1: one line per BASELINE config besides the headline, each measured the way the paper's
-    per-config numbers are quoted, with its roofline fraction and lnL parity."""
+    per-config numbers are quoted, with its roofline fraction, lnL parity and the SM
+    clocks sampled during its timed region."""
     from synth import gen
     subs = {}
-    plan = [("cfg1", 1, 500, 0.0, 5, 3, True), ("cfg2", 4096, 500, 0.0, 3, 2, False),
-            ("cfg3", 65536, 500, 0.0, 1, 1, False)]
-    for name, W, iters, tol, steps, warm, lat in plan:
+
+    def windows_sub(name, W, iters, tol, steps, warm, lat):
         rc = gen.CONFIGS[name]
         cfg = fit_cfg_for(M, name, iters, tol, lat)
-        r = run_windows(M, rc, name, W, cfg, 1, 0, dev, steps, warm, True, args.seed, keep=True)
+        clk = ClockSampler(gpu_index)
+        r = run_windows(M, rc, name, W, cfg, 1, 0, dev, steps, warm, True, args.seed, clocks=clk, keep=True)
         d = r["data"]
         sub = {"workload": f"{name}: {W} windows, D={rc.D}, ~{r['local_E'] // max(W, 1)} events/window, T={rc.T}s, "
                            + ("plain GD lr 0.5 on the mean loss" if name == "cfg1" else "Adam lr 0.05")
-                           + f", {iters} fixed iterations + final eval"
+                           + (f", {iters} fixed iterations + final eval" if tol <= 0 else
+                              f", converged mode: tol_rel {tol:g}, patience 10, at most {iters} iterations "
+                              f"(mean {r['mean_iters']:.1f}) + final eval")
                            + (", latency mode (one window per warp in 16 time chunks)" if lat else ""),
                "value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
                "windows_fitted_per_s": r["windows_fitted_per_s"], "fit_ms": r["fit_ms"],
-               "roofline": roofline_of(rc.D, r["local_ev_eval"], r["fit_ms"], "k_fit")}
+               "roofline": roofline_of(rc.D, r["local_ev_eval"], r["fit_ms"],
+                                       "k_fit_tc" if lat else "k_fit (refill)" if tol > 0 else "k_fit"),
+               "clocks": r["clocks"]}
         if name == "cfg1":
             sub["latency_ms_per_window_fit"] = r["fit_ms"]
             sub["us_per_iteration"] = 1e3 * r["fit_ms"] / (iters + 1)
         if not args.no_cpu:
             sub["parity"] = oracle_lnl_parity(rc.D, d, strided(W, 4096 if name != "cfg3" else 1024))
-        subs[name] = sub
-        del r, d
+        return sub
+
+    subs["cfg1"] = windows_sub("cfg1", 1, 500, 0.0, 5, 3, True)
+    subs["cfg2"] = windows_sub("cfg2", 4096, 500, 0.0, 3, 2, False)
     rc = gen.CONFIGS["cfg4"]
-    o = run_seq(M, rc, 500, 3, 2, args.seed, 0, dev, parity=not args.no_cpu)
+    clk = ClockSampler(gpu_index)
+    clk.start()
+    o = run_seq(M, rc, 500, 3, 2, args.seed, 0, dev, parity=False)
+    o["clocks"] = clk.stop()
+    if not args.no_cpu:
+        o.update(run_seq_parity(o))
+    o.pop("state", None)
     o["workload"] = f"cfg4: one sequence, D={rc.D}, {o['events']} events, chunked scan, Adam lr 0.05, 500 fixed iterations"
     subs["cfg4"] = o
+    subs["cfg3"] = windows_sub("cfg3", 65536, 500, 0.0, 1, 1, False)
     # cfg5 converged mode (SURVEY 8(d)): tol_rel 1e-6, patience 10, at most 500 iterations
-    rc = gen.CONFIGS["cfg5"]
-    cfg = fit_cfg_for(M, "cfg5", 500, 1e-6)
-    r = run_windows(M, rc, "cfg5", 1 << 20, cfg, 1, 0, dev, 1, 1, True, args.seed, keep=True)
-    sub = {"workload": "cfg5 converged mode: 1,048,576 windows, D=16, Adam lr 0.05, tol_rel 1e-6, patience 10, "
-                       f"at most 500 iterations (mean {r['mean_iters']:.1f}) + final eval",
-           "value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
-           "windows_fitted_per_s": r["windows_fitted_per_s"], "fit_ms": r["fit_ms"],
-           "roofline": roofline_of(16, r["local_ev_eval"], r["fit_ms"], "k_fit (refill)")}
-    if not args.no_cpu:
-        sub["parity"] = oracle_lnl_parity(16, r["data"], strided(1 << 20, 4096))
-    subs["cfg5_converged"] = sub
+    subs["cfg5_converged"] = windows_sub("cfg5", 1 << 20, 500, 1e-6, 1, 1, False)
     return subs
 
 
@@ -812,7 +823,7 @@ def main():
     del d, res["data"]
     torch.cuda.empty_cache()
     if world == 1 and not args.no_sub and args.config == "cfg5" and args.tol <= 0:
-        subs = sub_results(M, args, dev)
+        subs = sub_results(M, args, dev, clocks.idx)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
