@@ -848,6 +848,7 @@ def main():
                        "parallelism": (f"one batch split over {world} GPU(s) (balanced_ranges), final NCCL "
                                        "gather + reassembly on rank 0" if strong else
                                        f"weak: {W} windows per GPU, final NCCL gather"),
+                       "pack_and_gather_ms_per_step": res["ms_per_step"] - res["fit_ms"],
                        "per_rank": res["per_rank"], "imbalance_fit_max_over_mean": res["imbalance"],
                        "fit_ms_max_over_ranks": res["fit_ms_max_over_ranks"]},
             "windows_fitted_per_s": res["windows_fitted_per_s"],

@@ -217,7 +217,10 @@ typedef struct {
  *                OR-ed with this call's NONFINITE / DIVERGED / CONVERGED (outcome bits of an
  *                earlier call on the same batch are not carried over)
  *   lnl_trace [W][max_iters] fp32 out or NULL: lnL of every evaluation (NaN after the stop)
- * One persistent kernel launch for the iteration loop (+1 for workspace init).  Asynchronous.
+ * One persistent kernel launch for the iteration loop (+1 for the fp64 re-evaluation of
+ * cancellation windows).  Each CTA allocates tensor memory (TMEM) for the windows' optimizer
+ * state (pow2(7 Dp + 3) columns; 128 at D = 16) and frees it before it exits; kernels of other
+ * streams that hold TMEM on the same SMs can delay it.  Asynchronous.
  */
 int mdhp_fit(const mdhp_pack_desc* desc, const void* packed, const mdhp_fit_config* cfg,
              float* theta, float* alpha, float* beta, float* opt_state,
