@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--hidden", type=int, default=128, help="--config feat: MDHP-LSTM hidden size H")
     ap.add_argument("--latency", action="store_true",
                     help="mdhp_fit latency mode (D <= 8): one window per warp in time chunks")
+    ap.add_argument("--time-chunks", type=int, default=0,
+                    help="mdhp_fit time chunks per window (D <= 8; 0 = throughput layout)")
     ap.add_argument("--shard-seq", action="store_true",
                     help="cfg4: split ONE sequence over the ranks (f1, strong scaling, NCCL map exchange)")
     return ap.parse_args()
@@ -260,14 +262,15 @@ def bench_seq_sharded(args, rc, world, rank, dev):
     return 0
 
 
-def fit_cfg_for(M, name, iters, tol, latency=False):
+def fit_cfg_for(M, name, iters, tol, latency=False, time_chunks=0):
     """The fit each config is quoted on: cfg1 500 plain GD iterations on the mean loss (SURVEY
     8(d)), single-window latency in latency mode; the others Adam lr 0.05, fixed
     iterations or converged mode."""
     if name == "cfg1":
         return M.FitConfig(max_iters=iters, optimizer="gd", lr=0.5, loss="mean", tol_rel=tol, patience=10,
-                           latency_mode=latency)
-    return M.FitConfig(max_iters=iters, optimizer="adam", lr=0.05, tol_rel=tol, patience=10, latency_mode=latency)
+                           latency_mode=latency, time_chunks=time_chunks)
+    return M.FitConfig(max_iters=iters, optimizer="adam", lr=0.05, tol_rel=tol, patience=10, latency_mode=latency,
+                       time_chunks=time_chunks)
 
 
 def gen_batch(rc, name, W, seed, first, dev):
@@ -777,7 +780,7 @@ def main():
         return bench_loglik(args, rc, b, W, world, rank, dev)
 
     strong = not args.weak
-    cfg = fit_cfg_for(M, args.config, args.iters, args.tol, args.latency)
+    cfg = fit_cfg_for(M, args.config, args.iters, args.tol, args.latency, args.time_chunks)
     clocks = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
                           int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
     res = run_windows(M, rc, args.config, W, cfg, world, rank, dev, args.steps, args.warmup, strong,

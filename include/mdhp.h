@@ -193,12 +193,14 @@ typedef struct {
                                from a returned opt_state; 0 for a fresh fit.  fit(k) then
                                fit(m, opt_state, adam_step0 = k) == fit(k + m) in fixed-
                                iteration mode (checkpoint / resume)        */
-    int32_t  latency_mode;  /* 0: throughput layout (32/Dp windows per warp);  1: latency mode
-                               for single windows and small batches, Dp <= 8 (D <= 8): one
-                               window per warp, its events cut into 32/Dp time chunks run in
-                               parallel (chunked scan inside the warp, DESIGN.md a6).  Results
-                               agree with mode 0 within fp32 rounding (different summation
-                               order), deterministically.  Ignored for D > 8.               */
+    int32_t  time_chunks;   /* 0 or 1: throughput layout (32/Dp windows per warp).  C >= 2, for
+                               D <= 8: each window's events are cut into C' = min(pow2 <= C,
+                               32/Dp) time chunks run in parallel by C' lane groups (chunked
+                               scan inside the warp, DESIGN.md a6), 32/(Dp C') windows per warp:
+                               shorter per-window chains for single windows (latency mode,
+                               C' = 32/Dp: one window per warp) and small batches.  Results
+                               agree with C = 0 within fp32 rounding (another fixed summation
+                               order), deterministically.  Ignored for D > 8.                */
 } mdhp_fit_config;
 
 /*

@@ -130,7 +130,7 @@ static FitCfgDev to_dev(const mdhp_fit_config* cfg) {
   c.patience = cfg->patience;
   c.max_halvings = cfg->max_halvings;
   c.step0 = cfg->adam_step0;
-  c.latency = cfg->latency_mode;
+  c.time_chunks = cfg->time_chunks;
   c.lr = cfg->lr;
   c.b1 = cfg->adam_b1;
   c.b2 = cfg->adam_b2;
@@ -148,7 +148,7 @@ static int check_cfg(const mdhp_fit_config* c) {
   }
   if (c->max_iters < 0 || !(c->lr > 0.0f) || (c->optimizer != MDHP_OPT_GD && c->optimizer != MDHP_OPT_ADAM) ||
       !(c->min_param > 0.0f) || c->patience < 0 || c->max_halvings < 0 || c->adam_step0 < 0 ||
-      c->latency_mode < 0 || c->latency_mode > 1 ||
+      c->time_chunks < 0 ||
       (c->optimizer == MDHP_OPT_ADAM && !(c->adam_b1 >= 0.0f && c->adam_b1 < 1.0f &&
                                           c->adam_b2 >= 0.0f && c->adam_b2 < 1.0f && c->adam_eps >= 0.0f))) {
     set_error("invalid fit config");
@@ -372,7 +372,7 @@ int mdhp_fit(const mdhp_pack_desc* d, const void* packed, const mdhp_fit_config*
   c.patience = cfg->patience;
   c.max_halvings = cfg->max_halvings;
   c.step0 = cfg->adam_step0;
-  c.latency = cfg->latency_mode;
+  c.time_chunks = cfg->time_chunks;
   c.lr = cfg->lr;
   c.b1 = cfg->adam_b1;
   c.b2 = cfg->adam_b2;

@@ -244,7 +244,7 @@ struct FitCfgDev {
   float lr, b1, b2, eps, tol_rel, min_param;
   unsigned fit_mask;
   int step0;   // Adam steps of earlier calls (resume)
-  int latency; // latency mode (k_fit_tc): one window per warp in time chunks
+  int time_chunks;   // time chunks per window (k_fit_tc), 0/1 = throughput layout
 };
 
 // launch counter (process-wide), incremented by every launch site

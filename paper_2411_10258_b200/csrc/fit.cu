@@ -626,42 +626,43 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
   tm_free(tbase, TL::ALLOC);
 }
 
-// ---------------------------------------------------------------- latency mode (time chunks)
-// mdhp_fit_config.latency_mode, Dp <= 8: ONE window per warp, its events cut into G = 32/Dp
+// ---------------------------------------------------------------- time chunks (latency mode)
+// mdhp_fit_config.time_chunks = C >= 2, Dp <= 8: each window's events are cut into C
 // consecutive time chunks (boundaries on 8-event blocks, never inside a tie group), one per
-// group of Dp lanes, so a window's sequential event chain is ~G times shorter (single windows
-// and small batches, BASELINE cfg1).  Per evaluation (the a7 chunked scan inside a warp):
+// group of Dp lanes, so a warp holds 32/(Dp C) windows and a window's sequential event chain
+// is ~C times shorter.  C = 32/Dp (one window per warp) is the latency mode for single windows
+// (BASELINE cfg1); smaller C trades chain length against windows per warp for small batches.
+// Per evaluation (the a7 chunked scan inside a warp):
 //   phase 1: every group runs its chunk's column updates from a zero state (local_loop) and
 //            re-anchors the local state at the chunk's last event t_e;
-//   scan:    the affine maps of the chunks (decay over the chunk span + local state,
-//            seq.cu AffMap) are scanned across the groups with warp shuffles; the state
-//            carried into chunk g is the composite of chunks 0..g-1, anchored at the chunk
-//            base t_b (the previous chunk's last event);
+//   scan:    the affine maps of a window's chunks (decay over the chunk span + local state,
+//            seq.cu AffMap) are scanned across its groups with warp shuffles; the state carried
+//            into chunk q is the composite of chunks 0..q-1, anchored at the chunk base t_b (the
+//            previous chunk's last event);
 //   phase 3: every group runs the full event loop of its chunk from the carried state;
-//   then the groups' gradient accumulators, sum ln lambda and sum 1/lambda are added in a fixed
-//   order (identical in every group) and every group finishes the epilogue from the last
-//   chunk's final state, so all groups hold the same lnL, gradients and (after opt_action)
-//   parameters.  Results equal the plain kernel's within fp32 rounding (a different but fixed
-//   summation order), deterministic run to run.
+//   then a window's gradient accumulators, sum ln lambda and sum 1/lambda are added over its
+//   groups in a fixed order (identical in every group) and every group finishes the epilogue
+//   from the window's last chunk's final state, so all groups of a window hold the same lnL,
+//   gradients and (after opt_action) parameters.  Results equal the throughput layout's within
+//   fp32 rounding (a different but fixed summation order), deterministic run to run.
 struct TcChunk {
   int b, n;           // first event (relative to the window) and count of this group's chunk
   int clampo;         // offset of the window's null chunk, relative to b
   float tb, te;       // chunk base (last event before it, -1 if none) and last event time
 };
 
-template <int DP>
-__device__ __forceinline__ TcChunk tc_chunk(const Packed& P, int64_t beg, int n, int g) {
-  constexpr int G = 32 / DP;
-  // boundaries b_0 = 0 <= b_1 <= ... <= b_G = n: near k n / G, on 8-event blocks, moved past
+template <int CPW>
+__device__ __forceinline__ TcChunk tc_chunk(const Packed& P, int64_t beg, int n, int q) {
+  // boundaries b_0 = 0 <= b_1 <= ... <= b_C = n: near k n / C, on 8-event blocks, moved past
   // cross-mark tie groups (a chunk must not start at a time equal to its base)
   int lo = 0, hi = n;
   int prev = 0;
-  for (int k = 1; k <= g + 1 && k <= G; k++) {
-    int b = k == G ? n : (int)(((int64_t)n * k / G) & ~(int64_t)7);
+  for (int k = 1; k <= q + 1 && k <= CPW; k++) {
+    int b = k == CPW ? n : (int)(((int64_t)n * k / CPW) & ~(int64_t)7);
     if (b < prev) b = prev;
     while (b > 0 && b < n && P.t32[beg + b] == P.t32[beg + b - 1]) b = min(b + 8, n);
-    if (k == g) lo = b;
-    if (k == g + 1) hi = b;
+    if (k == q) lo = b;
+    if (k == q + 1) hi = b;
     prev = b;
   }
   TcChunk ch;
@@ -685,14 +686,18 @@ __device__ __forceinline__ TcMap tc_compose(const TcMap& m1, const TcMap& m2) {
   return r;
 }
 
-template <int DP, bool GRAD>
+// Evaluation of the window whose chunk q (= c.g % CPW) this group holds; see above.
+template <int DP, int CPW, bool GRAD>
 __device__ __forceinline__ double eval_window_tc(const Packed& P, float2* A, float2* SQ,
                                                  float2* Gs, float2* wbase, const WarpCtx<DP>& c,
                                                  int64_t w, bool live, const TcChunk& ch,
                                                  float th, const ColInfo& ci, float& dth,
                                                  bool& finite, bool& exact) {
   using SM = Smem<DP>;
-  constexpr int G = SM::G;
+  constexpr int WL = DP * CPW;                 // lanes of one window
+  const int q = c.g % CPW;                     // this group's chunk of its window
+  const int g0 = c.g - q;                      // the window's first group
+  const unsigned wmask = WL == 32 ? kFull : (((1u << WL) - 1u) << (g0 * DP));
   const int64_t beg = live ? P.begin[w] : 0;
   const int n = live ? ch.n : 0;
   const int nmax = group_max_i<DP>(n);
@@ -717,9 +722,9 @@ __device__ __forceinline__ double eval_window_tc(const Packed& P, float2* A, flo
     m[r].Sb = e * sq.x;
     m[r].Qb = e * fmaf(dl, sq.x, sq.y);
   }
-  // ---- inclusive scan of the maps over the groups (lane j of group g <- lane j of g - k)
+  // ---- inclusive scan of the maps over the window's groups (lane j of chunk q <- q - k)
 #pragma unroll
-  for (int k = 1; k < G; k <<= 1) {
+  for (int k = 1; k < CPW; k <<= 1) {
 #pragma unroll
     for (int r = 0; r < DP; r++) {
       TcMap up;
@@ -727,17 +732,17 @@ __device__ __forceinline__ double eval_window_tc(const Packed& P, float2* A, flo
       up.L = __shfl_up_sync(kFull, m[r].L, k * DP);
       up.Sb = __shfl_up_sync(kFull, m[r].Sb, k * DP);
       up.Qb = __shfl_up_sync(kFull, m[r].Qb, k * DP);
-      if (c.g >= k) m[r] = tc_compose(up, m[r]);
+      if (q >= k) m[r] = tc_compose(up, m[r]);
     }
   }
   // ---- phase 3: the full event loop of the chunk from the carried state (the composite of
-  // the earlier chunks applied to the empty initial state), anchored at tb
+  // the window's earlier chunks applied to the empty initial state), anchored at tb
   __syncwarp();
 #pragma unroll
   for (int r = 0; r < DP; r++) {
     const float cs = __shfl_up_sync(kFull, m[r].Sb, DP);
     const float cq = __shfl_up_sync(kFull, m[r].Qb, DP);
-    SQ[SM::e(r, c.j)] = c.g > 0 ? make_float2(cs, cq) : make_float2(0.0f, 0.0f);
+    SQ[SM::e(r, c.j)] = q > 0 ? make_float2(cs, cq) : make_float2(0.0f, 0.0f);
     Gs[SM::ge(r, c.j)] = make_float2(0.0f, 0.0f);
   }
   __syncwarp();
@@ -746,11 +751,11 @@ __device__ __forceinline__ double eval_window_tc(const Packed& P, float2* A, flo
   event_loop<DP, GRAD, true, true>(A, SQ, Gs, c.j, c.gbase, P.t32, P.dtp, P.mark, beg + ch.b, n,
                                    nmax, th, last, gth, lsum, ch.b > 0 ? ch.tb : -1.0f,
                                    ch.clampo, ch.tb);
-  // ---- sums over the chunks, in the same order in every group
+  // ---- sums over the window's chunks, in the same order in every group of the window
 #pragma unroll
-  for (int o = DP; o < 32; o <<= 1) gth += __shfl_xor_sync(kFull, gth, o);
+  for (int o = DP; o < WL; o <<= 1) gth += __shfl_xor_sync(kFull, gth, o);
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) lsum += __shfl_xor_sync(kFull, lsum, o);
+  for (int o = WL / 2; o >= 1; o >>= 1) lsum += __shfl_xor_sync(kFull, lsum, o);
   __syncwarp();
   float2 gtot[DP];
   if (GRAD) {
@@ -758,18 +763,19 @@ __device__ __forceinline__ double eval_window_tc(const Packed& P, float2* A, flo
     for (int r = 0; r < DP; r++) {
       float2 a = make_float2(0.0f, 0.0f);
 #pragma unroll
-      for (int q = 0; q < G; q++) {
-        const float2 v = (wbase + SM::group_off(q) + 2 * SM::AS)[SM::ge(r, c.j)];
+      for (int qq = 0; qq < CPW; qq++) {
+        const float2 v = (wbase + SM::group_off(g0 + qq) + 2 * SM::AS)[SM::ge(r, c.j)];
         a.x += v.x;
         a.y += v.y;
       }
       gtot[r] = a;
     }
   }
-  // ---- epilogue from the last chunk's final state (its SQ and its lanes' last times)
-  const float2* SQl = wbase + SM::group_off(G - 1) + SM::AS;
+  // ---- epilogue from the window's last chunk's final state (its SQ, its lanes' last times)
+  const int gl = g0 + CPW - 1;
+  const float2* SQl = wbase + SM::group_off(gl) + SM::AS;
   ColInfo cc = ci;
-  cc.last = __shfl_sync(kFull, last, (G - 1) * DP + c.j);
+  cc.last = __shfl_sync(kFull, last, gl * DP + c.j);
   Series S;
   load_series(S, P.mom + ((size_t)(live ? w : 0) * P.Dp + c.j) * kMom, live && cc.N > 0);
   double part3 = 0.0;
@@ -803,14 +809,15 @@ __device__ __forceinline__ double eval_window_tc(const Packed& P, float2* A, flo
   part3 = group_sum_d<DP>(part3);
   const double sth = group_sum_d<DP>(cc.real ? (double)th : 0.0);
   const double lnl = (double)kLn2 * lsum + part3 - (double)ci.T * sth;
-  finite = __all_sync(kFull, ok) && isfinite(lnl);
+  const unsigned bal = __ballot_sync(kFull, ok) & wmask;
+  finite = (bal == wmask) && isfinite(lnl);
   const int ntot = live ? P.n[w] : 0;
   exact = live && needs_exact(lnl, ntot, (double)kLn2 * lsum, (double)ci.T * sth, part3);
   __syncwarp();
   return lnl;
 }
 
-template <int DP, bool RESUME>
+template <int DP, int CPW, bool RESUME>
 __global__ void __launch_bounds__(128, 4)
 k_fit_tc(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ alpha,
          float* __restrict__ beta, float* __restrict__ opt, double* __restrict__ lnl_out,
@@ -820,7 +827,8 @@ k_fit_tc(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__
   extern __shared__ __align__(16) unsigned char smem[];
   using SM = Smem<DP>;
   using TL = TmCols<DP>;
-  static_assert(DP <= 8, "latency mode: Dp <= 8");
+  static_assert(DP <= 8 && CPW >= 2 && CPW * DP <= 32, "time chunks: Dp <= 8, 2 <= C <= 32/Dp");
+  constexpr int WPW = 32 / (DP * CPW);   // windows per warp
   WarpCtx<DP> c;
   const int wid = threadIdx.x >> 5;
   float2* wbase = reinterpret_cast<float2*>(smem + wid * SM::per_warp);
@@ -831,45 +839,50 @@ k_fit_tc(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__
   const uint32_t tbase = tm_alloc(slot, TL::ALLOC);
   const uint32_t tm = tbase + ((uint32_t)((wid & 3) * 32) << 16);
   const int D = P.D;
+  const int q = c.g % CPW;
+  const bool first_lane = (c.lane % (DP * CPW)) == 0;   // the window's lane 0
+  const int64_t nunits = (P.W + WPW - 1) / WPW;
   for (;;) {
     int64_t unit = 0;
     if (c.lane == 0) unit = atomicAdd(counter, 1);
     unit = __shfl_sync(kFull, unit, 0);
-    if (unit >= P.W) break;
-    const int64_t w = P.perm[unit];
-    MDHP_ASSERT(w >= 0 && w < P.W);
-    const int st0 = status[w];
-    const bool live = !(st0 & MDHP_ST_INVALID);
+    if (unit >= nunits) break;
+    const int64_t slot_w = unit * WPW + c.g / CPW;
+    const int64_t w = slot_w < P.W ? P.perm[slot_w] : 0;
+    MDHP_ASSERT(w >= 0 && w < (P.W > 0 ? P.W : 1));
+    const int st0 = slot_w < P.W ? status[w] : MDHP_ST_INVALID;
+    const bool live = slot_w < P.W && !(st0 & MDHP_ST_INVALID);
     float th = load_window<DP>(A, c, D, w, true, live, tm, 0.0f, theta, alpha, beta, opt);
     const ColInfo ci = col_info<DP>(P, w, live, c.j);
     const int n = live ? P.n[w] : 0;
-    const TcChunk ch = tc_chunk<DP>(P, live ? P.begin[w] : 0, n, c.g);
+    const TcChunk ch = tc_chunk<CPW>(P, live ? P.begin[w] : 0, n, q);
     const float scale = (cfg.loss_mean && n > 0) ? 1.0f / (float)n : 1.0f;
     WinCtl ctl;
     ctl.lr_w = cfg.lr;
     bool done = !live || cfg.max_iters <= 0;
-    while (!done) {   // one window per warp: warp-uniform
+    while (__any_sync(kFull, !done)) {   // windows of a warp stop independently (mask)
       float dth;
       bool finite, exact;
-      const double lnl = eval_window_tc<DP, true>(P, A, SQ, Gs, wbase, c, w, live, ch, th, ci, dth,
-                                                  finite, exact);
-      const int act = ctl.decide(cfg, lnl, finite, done, trace, w, c.lane == 0);
-      if (act != ACT_NONE)
+      const double lnl = eval_window_tc<DP, CPW, true>(P, A, SQ, Gs, wbase, c, w, live && !done, ch,
+                                                       th, ci, dth, finite, exact);
+      int act = ACT_NONE;
+      if (!done) act = ctl.decide(cfg, lnl, finite, done, trace, w, first_lane);
+      if (__any_sync(kFull, act != ACT_NONE))
         opt_action<DP, RESUME>(A, Gs, c, D, cfg, act, ctl.lr_w, ctl.s, scale, dth, th, tm);
       __syncwarp();
     }
     float dth;
     bool finite, exact;
-    const double lnl = eval_window_tc<DP, false>(P, A, SQ, Gs, wbase, c, w, live, ch, th, ci, dth,
-                                                 finite, exact);
-    store_window<DP>(A, c, D, w, live && c.g == 0, th, tm, theta, alpha, beta, opt);
-    if (c.lane == 0) {
+    const double lnl = eval_window_tc<DP, CPW, false>(P, A, SQ, Gs, wbase, c, w, live, ch, th, ci,
+                                                      dth, finite, exact);
+    store_window<DP>(A, c, D, w, slot_w < P.W && live && q == 0, th, tm, theta, alpha, beta, opt);
+    if (slot_w < P.W && first_lane) {
       lnl_out[w] = live ? lnl : (double)NAN;
       iters_out[w] = ctl.it;
       status[w] = (st0 & kKeepStatus) | ctl.st;
       if (exact) list_exact(xlist, xcount, w);
       if (trace && live)
-        for (int q = ctl.it; q < cfg.max_iters; q++) trace[(size_t)w * cfg.max_iters + q] = NAN;
+        for (int k = ctl.it; k < cfg.max_iters; k++) trace[(size_t)w * cfg.max_iters + k] = NAN;
     }
     __syncwarp();
   }
@@ -923,12 +936,20 @@ static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float*
   // converged mode (tol_rel > 0): windows stop at different iterations -> per-window refill
   auto kern = cfg.tol_rel > 0.0f ? (cfg.step0 != 0 ? k_fit<DP, true, true> : k_fit<DP, false, true>)
                                  : (cfg.step0 != 0 ? k_fit<DP, true, false> : k_fit<DP, false, false>);
-  // latency mode (Dp <= 8): one window per warp, its events in 32/Dp time chunks (k_fit_tc)
-  bool tc = false;
+  // time chunks (Dp <= 8): C chunks per window, 32/(Dp C) windows per warp (k_fit_tc)
+  int cpw = 1;
   if constexpr (DP <= 8) {
-    if (cfg.latency) {
-      kern = cfg.step0 != 0 ? k_fit_tc<DP, true> : k_fit_tc<DP, false>;
-      tc = true;
+    if (cfg.time_chunks >= 2) {
+      cpw = 2;
+      while (cpw * 2 <= cfg.time_chunks && cpw * 2 * DP <= 32) cpw *= 2;
+      const bool rs = cfg.step0 != 0;
+      switch (cpw) {
+        case 2: kern = rs ? k_fit_tc<DP, 2, true> : k_fit_tc<DP, 2, false>; break;
+        case 4: kern = rs ? k_fit_tc<DP, (DP <= 8 ? 4 : 2), true> : k_fit_tc<DP, (DP <= 8 ? 4 : 2), false>; break;
+        case 8: kern = rs ? k_fit_tc<DP, (DP <= 4 ? 8 : 2), true> : k_fit_tc<DP, (DP <= 4 ? 8 : 2), false>; break;
+        case 16: kern = rs ? k_fit_tc<DP, (DP <= 2 ? 16 : 2), true> : k_fit_tc<DP, (DP <= 2 ? 16 : 2), false>; break;
+        default: kern = rs ? k_fit_tc<DP, (DP <= 1 ? 32 : 2), true> : k_fit_tc<DP, (DP <= 1 ? 32 : 2), false>; break;
+      }
     }
   }
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -961,7 +982,8 @@ static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float*
     fprintf(stderr, "k_fit<%d>: per_sm=%d (regs %d smem %d tmem %d) smem=%zu regs=%d local=%zu\n", DP,
             per_sm, by_regs, by_smem, by_tmem, smem, fa.numRegs, fa.localSizeBytes);
   if (per_sm < 1) per_sm = 1;
-  const int64_t units = tc ? P.W : (P.W + SM::G - 1) / SM::G;
+  const int64_t wpu = cpw > 1 ? SM::G / cpw : SM::G;   // windows per warp unit
+  const int64_t units = (P.W + wpu - 1) / wpu;
   int64_t blocks = (int64_t)sms * per_sm;
   const int64_t need = (units + WPB - 1) / WPB;
   if (blocks > need) blocks = need;

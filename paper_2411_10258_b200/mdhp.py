@@ -44,7 +44,7 @@ class FitConfigC(ctypes.Structure):
                 ("tol_rel", ctypes.c_float), ("patience", ctypes.c_int32),
                 ("min_param", ctypes.c_float), ("fit_mask", ctypes.c_uint32),
                 ("max_halvings", ctypes.c_int32), ("adam_step0", ctypes.c_int32),
-                ("latency_mode", ctypes.c_int32)]
+                ("time_chunks", ctypes.c_int32)]
 
 
 @dataclass
@@ -64,13 +64,14 @@ class FitConfig:
     fit_mask: int = 7
     max_halvings: int = 8
     adam_step0: int = 0        # Adam steps already taken when resuming from a returned opt_state
-    latency_mode: bool = False  # one window per warp in time chunks (D <= 8; single windows)
+    time_chunks: int = 0        # time chunks per window (D <= 8): 0 = throughput layout
+    latency_mode: bool = False  # shorthand for the most time chunks (one window per warp)
 
     def c(self) -> FitConfigC:
         return FitConfigC(self.max_iters, OPT_ADAM if self.optimizer == "adam" else OPT_GD,
                           self.lr, self.b1, self.b2, self.eps, 1 if self.loss == "mean" else 0,
                           self.tol_rel, self.patience, self.min_param, self.fit_mask,
-                          self.max_halvings, self.adam_step0, 1 if self.latency_mode else 0)
+                          self.max_halvings, self.adam_step0, 32 if self.latency_mode else self.time_chunks)
 
 
 _lib = None

@@ -613,3 +613,32 @@ def test_fit_latency_mode_converged_and_resume():
     for x, y in zip(a_, c_):
         assert torch.equal(x, y)
     assert torch.equal(opt_a, opt_c) and torch.equal(ra["lnl"], rc["lnl"])
+
+
+@pytest.mark.parametrize("D,tc", [(2, 2), (2, 4), (3, 2), (5, 2), (8, 2), (8, 4)])
+def test_fit_time_chunks_vs_oracle(D, tc):
+    """time_chunks = C (several windows per warp, each cut into C time chunks): fitted
+    parameters within R17 and lnL within 1e-4 of the oracle's fit; ragged window lengths in one
+    warp (windows of a warp finish their chunks at different times), empty and tiny windows."""
+    b, _ = H.small_batch(D, 23, seed=950 + D, edges=True)
+    W = len(b["T"])
+    rng = np.random.default_rng(D + tc)
+    th0 = rng.uniform(0.5, 5.0, (W, D)); al0 = rng.uniform(0.0, 3.0, (W, D, D)); be0 = rng.uniform(2.0, 40.0, (W, D, D))
+    kw = dict(max_iters=20, optimizer="adam", lr=0.02, tol_rel=0.0)
+    pk = M.pack_windows(D, *dev_batch(b))
+    tt = [torch.tensor(f32(x), device=DEV) for x in (th0, al0, be0)]
+    r = M.fit(pk, *tt, M.FitConfig(time_chunks=tc, **kw))
+    torch.cuda.synchronize()
+    t32, T32, st = H.oracle_times(b, D)
+    for w in range(W):
+        if st[w] & oracle.INVALID_MASK:
+            continue
+        a, z = b["win_off"][w], b["win_off"][w + 1]
+        o = oracle.fit(D, t32[a:z], b["mark"][a:z], T32[w], f32(th0[w]).astype(float), f32(al0[w]).astype(float),
+                       f32(be0[w]).astype(float), oracle.FitConfig(**kw))
+        assert int(r["iters"][w]) == o["iters"]
+        for got, ref in ((tt[0][w], o["theta"]), (tt[1][w], o["alpha"]), (tt[2][w], o["beta"])):
+            got = got.cpu().numpy().astype(np.float64)
+            s = 1e-2 * max(np.mean(np.abs(ref)), 1e-4)
+            assert np.all(np.abs(got - ref) <= 1e-3 * np.maximum(np.abs(ref), s)), (D, tc, w, got, ref)
+        assert abs(float(r["lnl"][w]) - o["lnl"]) <= 1e-4 * abs(o["lnl"]), (D, tc, w)
