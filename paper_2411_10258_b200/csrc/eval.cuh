@@ -60,8 +60,14 @@ struct Smem {
   static constexpr int AS = (DP + 1) * RS;          // float2 from A to SQ (and SQ to G): DP
                                                     // real rows + the null row DP
   static constexpr int GS = SW ? AS : (DP + 1) * DP;   // float2 of G (+ null row)
+  // DP = 8: NGC copies of G, event s of a chunk accumulating into copy s % NGC, so pass 2's
+  // read-modify-writes of NGC consecutive events are independent and issue together (the
+  // serial LDS -> FFMA -> STS chain of the 8 events was ~30% of the latency-bound cfg2 loop,
+  // profiles/r02_cfg2_*); readers add the copies (gsum).  At DP = 16/32 the kernels are bound
+  // by shared-memory throughput, not latency, and keep one copy.
+  static constexpr int NGC = DP == 8 ? 4 : 1;
   static constexpr int P = SW ? 16 / DP : 1;        // groups sharing one row block
-  static constexpr int per_group = 2 * AS + GS;     // float2 per group (SW: per block of P)
+  static constexpr int per_group = 2 * AS + NGC * GS;   // float2 per group (SW: per block of P)
   static constexpr size_t per_warp = (size_t)(G / P) * per_group * sizeof(float2);
   // float2 offset of group g's A from the warp's base
   __host__ __device__ static constexpr int group_off(int g) {
@@ -75,6 +81,27 @@ struct Smem {
     return SW ? r * 16 + ((c ^ r) & (DP - 1)) : r * DP + c;
   }
 };
+
+// Gradient accumulator (r, c) summed over the NGC copies (fixed order), and zeroing of all
+// copies.  Gs = the group's G base (A + 2 AS).
+template <int DP>
+__device__ __forceinline__ float2 gsum(const float2* Gs, int r, int c) {
+  using SM = Smem<DP>;
+  float2 a = Gs[SM::ge(r, c)];
+#pragma unroll
+  for (int k = 1; k < SM::NGC; k++) {
+    const float2 v = Gs[k * SM::GS + SM::ge(r, c)];
+    a.x += v.x;
+    a.y += v.y;
+  }
+  return a;
+}
+template <int DP>
+__device__ __forceinline__ void gzero(float2* Gs, int r, int c) {
+  using SM = Smem<DP>;
+#pragma unroll
+  for (int k = 0; k < SM::NGC; k++) Gs[k * SM::GS + SM::ge(r, c)] = make_float2(0.0f, 0.0f);
+}
 
 // Parameter pair order in A.  Half of the pairs are stored {beta, alpha} instead of
 // {alpha, beta}, chosen so that the 32-bit beta column read of the event loop hits even banks
@@ -118,7 +145,7 @@ __device__ __forceinline__ void reset_state(float2* SQ, float2* Gs, int j) {
 #pragma unroll
   for (int i = 0; i < DP; i++) {
     SQ[SM::e(i, j)] = make_float2(0.0f, 0.0f);
-    Gs[SM::ge(i, j)] = make_float2(0.0f, 0.0f);
+    gzero<DP>(Gs, i, j);
   }
   SQ[SM::e(DP, j)] = make_float2(j == 0 ? 1.0f : 0.0f, 0.0f);
   if constexpr (!SM::SW) SQ[SM::e(j, DP)] = make_float2(0.0f, 0.0f);
@@ -302,6 +329,29 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
   const uint32_t colbb = colb + (ab_swapped<DP>(j) ? 0u : 4u);
   float pv[8], Rv[8], Qv[8];
   float lacc = 0.0f;
+  // DP <= 8 (latency-bound: few warps per SM): the column decay factors ec of the chunk's 8
+  // events depend only on parameters (beta'_ji) and gaps, so their loads and exponentials are
+  // issued here, ahead of the chunk's state stores, which takes the beta load and the MUFU off
+  // the event-to-event chain (state load -> FFMA -> state store).  (ptxas cannot move the
+  // loads above the stores itself: it cannot prove the addresses disjoint.)
+  constexpr bool HOIST = DP <= 8;
+  float ecs[8];
+  if constexpr (HOIST) {
+#pragma unroll
+    for (int s = 0; s < 8; s++) {
+      const float t = s == 0 ? ck.ta.x : s == 1 ? ck.ta.y : s == 2 ? ck.ta.z : s == 3 ? ck.ta.w
+                    : s == 4 ? ck.tb.x : s == 5 ? ck.tb.y : s == 6 ? ck.tb.z : ck.tb.w;
+      float dc = s == 0 ? ck.da.x : s == 1 ? ck.da.y : s == 2 ? ck.da.z : s == 3 ? ck.da.w
+               : s == 4 ? ck.db.x : s == 5 ? ck.db.y : s == 6 ? ck.db.z : ck.db.w;
+      if constexpr (TC) dc = fminf(dc, t - tb);
+      (void)t;
+      const int i = (int)__byte_perm(s < 4 ? ck.mm.x : ck.mm.y, 0u, 0x4440u | (unsigned)(s & 3));
+      const uint32_t cab = SW ? colbb + (((uint32_t)(i ^ j) & (uint32_t)(DP - 1)) << 3)
+                              : colbb + ((uint32_t)i << 3);
+      const float bc = lda1o<0>(cab);
+      ecs[s] = PRE ? ex2f(bc * dc) : ex2f(bc * (dc * -kLog2e));
+    }
+  }
 #pragma unroll
   for (int s = 0; s < 8; s++) {
     const float t = s == 0 ? ck.ta.x : s == 1 ? ck.ta.y : s == 2 ? ck.ta.z : s == 3 ? ck.ta.w
@@ -326,15 +376,21 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
       ca = colb + ((uint32_t)i << 3);
       cab = colbb + ((uint32_t)i << 3);
     }
-    MDHP_ASSERT(ra + kG + 8 <= sA + 8u * (uint32_t)(3 * SM::AS) && ca + kSQ + 8 <= sA + 8u * (uint32_t)(3 * SM::AS));
+    MDHP_ASSERT(ra + 8 <= sA + 8u * (uint32_t)SM::AS && ca + kSQ + 8 <= sA + 8u * (uint32_t)(2 * SM::AS));
     const float2 ar = lda2(ra);
     const float2 sr = lds2o<kSQ>(ra);
-    const float bc = lda1o<0>(cab);
     const float2 sc = lds2o<kSQ>(ca);
     const float dr = t - last;
     const float a_ij = ab_alpha<DP>(i, ar), b_ij = ab_beta<DP>(i, ar);
     const float er = PRE ? ex2f(b_ij * dr) : ex2f(b_ij * (dr * -kLog2e));
-    const float ec = PRE ? ex2f(bc * dc) : ex2f(bc * (dc * -kLog2e));
+    float ec;
+    if constexpr (HOIST) {
+      ec = ecs[s];
+      (void)cab;
+    } else {
+      const float bc = lda1o<0>(cab);
+      ec = PRE ? ex2f(bc * dc) : ex2f(bc * (dc * -kLog2e));
+    }
     const float R = fmaf(er, sr.x, -fset_eq0(dr));   // strict T_j^k < t
     // theta_i enters after the reduction for DP >= 8 (below), through lane i for DP <= 4
     const float p = DP >= 8 ? a_ij * R : fmaf(a_ij, R, fsel_eqi(i, j, th, 0.0f));
@@ -352,7 +408,7 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
       if (GRAD) {
         const float w = rcpf(lam);
         const uint32_t ga = SW ? ra : rowb + ((uint32_t)i * (8u * DP));
-        MDHP_ASSERT(ga + kG + 8 <= sA + 8u * (uint32_t)(3 * SM::AS));
+        MDHP_ASSERT(ga + kG + 8 <= sA + 8u * (uint32_t)(2 * SM::AS + SM::GS));
         const float2 gg = lds2o<kG>(ga);
         sts2o<kG>(ga, fmaf(R, w, gg.x), fmaf(er * fmaf(dr, sr.x, sr.y), w, gg.y));
         gth += fsel_eqi(i, j, w, 0.0f);
@@ -387,23 +443,41 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
         wa = lds4(scr);
         wb = lds4(scr + 16u);
       }
+      // NGC consecutive events at a time, event s into copy s % NGC: their loads issue
+      // together, then their stores (the copies never alias)
+      constexpr int NGC = SM::NGC;
 #pragma unroll
-      for (int s = 0; s < 8; s++) {
-        const float ws = DP > 16 ? __shfl_sync(kFull, w, gbase + (s << (LG - 3)))
-                       : s == 0 ? wa.x : s == 1 ? wa.y : s == 2 ? wa.z : s == 3 ? wa.w
-                       : s == 4 ? wb.x : s == 5 ? wb.y : s == 6 ? wb.z : wb.w;
-        const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
-        // re-extract the mark (shift/mask, not pass 1's PRMT) so that pass 1's 8 "i == j"
-        // predicates are not kept live across the reduction (ptxas would pack them into a
-        // register with two LOP3 each)
-        const int i = (int)((word >> (8 * (s & 3))) & 0xffu);
-        MDHP_ASSERT(i >= 0 && i <= DP);
-        const uint32_t ga = SW ? (sA + kG) + (uint32_t)i * 128u + (((uint32_t)(i ^ j) & (uint32_t)(DP - 1)) << 3)
-                               : (rowb + kG) + ((uint32_t)i << (3 + LG));
-        MDHP_ASSERT(ga >= sA + kG && ga + 8 <= sA + 8u * (uint32_t)(3 * SM::AS));
-        const float2 gg = lds2(ga);
-        sts2o<0>(ga, fmaf(Rv[s], ws, gg.x), fmaf(Qv[s], ws, gg.y));
-        gth += fsel_eqi(i, j, ws, 0.0f);
+      for (int s0 = 0; s0 < 8; s0 += NGC) {
+        float2 gg[NGC];
+        uint32_t ga[NGC];
+        float wsv[NGC];
+#pragma unroll
+        for (int u = 0; u < NGC; u++) {
+          const int s = s0 + u;
+          wsv[u] = DP > 16 ? __shfl_sync(kFull, w, gbase + (s << (LG - 3)))
+                 : s == 0 ? wa.x : s == 1 ? wa.y : s == 2 ? wa.z : s == 3 ? wa.w
+                 : s == 4 ? wb.x : s == 5 ? wb.y : s == 6 ? wb.z : wb.w;
+          const unsigned word = s < 4 ? ck.mm.x : ck.mm.y;
+          // re-extract the mark (shift/mask, not pass 1's PRMT) so that pass 1's 8 "i == j"
+          // predicates are not kept live across the reduction (ptxas would pack them into a
+          // register with two LOP3 each)
+          const int i = (int)((word >> (8 * (s & 3))) & 0xffu);
+          MDHP_ASSERT(i >= 0 && i <= DP);
+          ga[u] = (SW ? (sA + kG) + (uint32_t)i * 128u + (((uint32_t)(i ^ j) & (uint32_t)(DP - 1)) << 3)
+                      : (rowb + kG) + ((uint32_t)i << (3 + LG))) + 8u * (uint32_t)(u * SM::GS);
+          MDHP_ASSERT(ga[u] >= sA + kG && ga[u] + 8 <= sA + 8u * (uint32_t)(2 * SM::AS + NGC * SM::GS));
+          gg[u] = lds2(ga[u]);
+          if constexpr (NGC > 1) gth += fsel_eqi(i, j, wsv[u], 0.0f);
+          else {
+            sts2o<0>(ga[u], fmaf(Rv[s], wsv[u], gg[u].x), fmaf(Qv[s], wsv[u], gg[u].y));
+            gth += fsel_eqi(i, j, wsv[u], 0.0f);
+          }
+        }
+        if constexpr (NGC > 1) {
+#pragma unroll
+          for (int u = 0; u < NGC; u++)
+            sts2o<0>(ga[u], fmaf(Rv[s0 + u], wsv[u], gg[u].x), fmaf(Qv[s0 + u], wsv[u], gg[u].y));
+        }
       }
     }
   }

@@ -73,7 +73,7 @@ __device__ __forceinline__ double eval_window(const Packed& P, float2* A, float2
     if (cc.real && i < P.D) {
       part3 += (double)(ka * Eb);
       if (GRAD) {
-        float2 gg = Gs[SM::ge(i, c.j)];
+        float2 gg = gsum<DP>(Gs, i, c.j);
         const float da = gg.x + Eb;
         const float db = fmaf(-ka, gg.y, ka * Hb2);
         ok = ok && isfinite(da) && isfinite(db);
@@ -743,7 +743,7 @@ __device__ __forceinline__ double eval_window_tc(const Packed& P, float2* A, flo
     const float cs = __shfl_up_sync(kFull, m[r].Sb, DP);
     const float cq = __shfl_up_sync(kFull, m[r].Qb, DP);
     SQ[SM::e(r, c.j)] = q > 0 ? make_float2(cs, cq) : make_float2(0.0f, 0.0f);
-    Gs[SM::ge(r, c.j)] = make_float2(0.0f, 0.0f);
+    gzero<DP>(Gs, r, c.j);
   }
   __syncwarp();
   float last, gth;
@@ -764,7 +764,7 @@ __device__ __forceinline__ double eval_window_tc(const Packed& P, float2* A, flo
       float2 a = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int qq = 0; qq < CPW; qq++) {
-        const float2 v = (wbase + SM::group_off(g0 + qq) + 2 * SM::AS)[SM::ge(r, c.j)];
+        const float2 v = gsum<DP>(wbase + SM::group_off(g0 + qq) + 2 * SM::AS, r, c.j);
         a.x += v.x;
         a.y += v.y;
       }

@@ -576,7 +576,7 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
       *a = ab_pack<DP>(i, 0.0f, 1.0f);
       SQ[SM::e(i, j)] = make_float2(0.0f, 0.0f);
     }
-    Gs[SM::ge(i, j)] = make_float2(0.0f, 0.0f);
+    gzero<DP>(Gs, i, j);
   }
   cp_async_wait_all();
   A[SM::e(DP, j)] = ab_pack<DP>(DP, j == 0 ? 1.0f : 0.0f, 0.0f);
@@ -622,7 +622,7 @@ k_seq_eval(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* 
       if (e < (int)(2 * DD)) {
         if (grad) {
           const int pr = e >> 1;
-          const float2 v = gb[2 * SM::AS + SM::ge(pr / D, pr % D)];
+          const float2 v = gsum<DP>(gb + 2 * SM::AS, pr / D, pr % D);
           acc += (double)((e & 1) ? v.y : v.x);
         }
       } else if (e < (int)(2 * DD) + D) {
