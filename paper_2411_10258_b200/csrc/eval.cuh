@@ -334,6 +334,25 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
   // issued here, ahead of the chunk's state stores, which takes the beta load and the MUFU off
   // the event-to-event chain (state load -> FFMA -> state store).  (ptxas cannot move the
   // loads above the stores itself: it cannot prove the addresses disjoint.)
+  // SW: the addresses of the chunk's 8 events come from two byte-parallel words per 4 events:
+  // y = 16 i + ((i ^ j) & (DP-1)) (the row element (i, j) in float2 units from the group base,
+  // <= 135, one byte) and x = 8 ((i ^ j) & (DP-1)) (the column element's byte offset), so an
+  // event needs one PRMT + one LEA/IADD per address instead of a PRMT-XOR-shift-mask-IMAD
+  // chain; y == 16 j exactly when i == j.
+  uint32_t yw[2] = {0u, 0u}, xw[2] = {0u, 0u};
+  const int j16 = 16 * j;
+  if constexpr (SW) {
+    const uint32_t J4 = (uint32_t)j * 0x01010101u;
+    constexpr uint32_t M4 = (uint32_t)(DP - 1) * 0x01010101u;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint32_t m4 = h == 0 ? ck.mm.x : ck.mm.y;
+      const uint32_t t4 = (m4 ^ J4) & M4;
+      yw[h] = (m4 << 4) | t4;   // marks <= 8: no carry across bytes
+      xw[h] = t4 << 3;
+    }
+  }
+  auto byte_of = [](uint32_t w, int s) -> uint32_t { return __byte_perm(w, 0u, 0x4440u | (unsigned)(s & 3)); };
   constexpr bool HOIST = DP <= 8;
   float ecs[8];
   if constexpr (HOIST) {
@@ -346,8 +365,7 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
       if constexpr (TC) dc = fminf(dc, t - tb);
       (void)t;
       const int i = (int)__byte_perm(s < 4 ? ck.mm.x : ck.mm.y, 0u, 0x4440u | (unsigned)(s & 3));
-      const uint32_t cab = SW ? colbb + (((uint32_t)(i ^ j) & (uint32_t)(DP - 1)) << 3)
-                              : colbb + ((uint32_t)i << 3);
+      const uint32_t cab = SW ? colbb + byte_of(xw[s >> 2], s) : colbb + ((uint32_t)i << 3);
       const float bc = lda1o<0>(cab);
       ecs[s] = PRE ? ex2f(bc * dc) : ex2f(bc * (dc * -kLog2e));
     }
@@ -366,11 +384,16 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     const int i = (int)__byte_perm(word, 0u, 0x4440u | (unsigned)(s & 3));   // mark (null: DP)
     MDHP_ASSERT(i >= 0 && i <= DP);
     uint32_t ra, ca, cab;
+    // ii: the mark for the i == j / null tests (SW: y, compared with 16 j / 16 DP)
+    int ii = i, jj = j, inull = DP;
     if constexpr (SW) {
-      const uint32_t x = ((uint32_t)(i ^ j) & (uint32_t)(DP - 1)) << 3;
-      ra = sA + (uint32_t)i * 128u + x;
+      const uint32_t y = byte_of(yw[s >> 2], s), x = byte_of(xw[s >> 2], s);
+      ra = sA + 8u * y;
       ca = colb + x;
       cab = colbb + x;
+      ii = (int)y;
+      jj = j16;
+      inull = 16 * DP;
     } else {
       ra = rowb + (uint32_t)i * (8u * RS);
       ca = colb + ((uint32_t)i << 3);
@@ -393,10 +416,10 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     }
     const float R = fmaf(er, sr.x, -fset_eq0(dr));   // strict T_j^k < t
     // theta_i enters after the reduction for DP >= 8 (below), through lane i for DP <= 4
-    const float p = DP >= 8 ? a_ij * R : fmaf(a_ij, R, fsel_eqi(i, j, th, 0.0f));
+    const float p = DP >= 8 ? a_ij * R : fmaf(a_ij, R, fsel_eqi(ii, jj, th, 0.0f));
     // SW: the null column has no storage; a null event's column update is not stored
-    if (!SW || i < DP) sts2o<kSQ>(ca, fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
-    last = fsel_eqi(i, j, t, last);
+    if (!SW || ii < inull) sts2o<kSQ>(ca, fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
+    last = fsel_eqi(ii, jj, t, last);
     if constexpr (DP >= 8) {
       pv[s] = p;
       if (GRAD) {
@@ -411,7 +434,7 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
         MDHP_ASSERT(ga + kG + 8 <= sA + 8u * (uint32_t)(2 * SM::AS + SM::GS));
         const float2 gg = lds2o<kG>(ga);
         sts2o<kG>(ga, fmaf(R, w, gg.x), fmaf(er * fmaf(dr, sr.x, sr.y), w, gg.y));
-        gth += fsel_eqi(i, j, w, 0.0f);
+        gth += fsel_eqi(ii, jj, w, 0.0f);
       }
       lacc += (j == 0) ? lg2f(lam) : 0.0f;
     }
@@ -461,16 +484,21 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
           // re-extract the mark (shift/mask, not pass 1's PRMT) so that pass 1's 8 "i == j"
           // predicates are not kept live across the reduction (ptxas would pack them into a
           // register with two LOP3 each)
-          const int i = (int)((word >> (8 * (s & 3))) & 0xffu);
+          int i = (int)((word >> (8 * (s & 3))) & 0xffu), jj = j;
           MDHP_ASSERT(i >= 0 && i <= DP);
-          ga[u] = (SW ? (sA + kG) + (uint32_t)i * 128u + (((uint32_t)(i ^ j) & (uint32_t)(DP - 1)) << 3)
-                      : (rowb + kG) + ((uint32_t)i << (3 + LG))) + 8u * (uint32_t)(u * SM::GS);
+          if constexpr (SW) {   // y (see above): the row element (i, j) of G
+            i = (int)byte_of(yw[s >> 2], s);
+            jj = j16;
+            ga[u] = (sA + kG + 8u * (uint32_t)(u * SM::GS)) + 8u * (uint32_t)i;
+          } else {
+            ga[u] = (rowb + kG) + ((uint32_t)i << (3 + LG)) + 8u * (uint32_t)(u * SM::GS);
+          }
           MDHP_ASSERT(ga[u] >= sA + kG && ga[u] + 8 <= sA + 8u * (uint32_t)(2 * SM::AS + NGC * SM::GS));
           gg[u] = lds2(ga[u]);
-          if constexpr (NGC > 1) gth += fsel_eqi(i, j, wsv[u], 0.0f);
+          if constexpr (NGC > 1) gth += fsel_eqi(i, jj, wsv[u], 0.0f);
           else {
             sts2o<0>(ga[u], fmaf(Rv[s], wsv[u], gg[u].x), fmaf(Qv[s], wsv[u], gg[u].y));
-            gth += fsel_eqi(i, j, wsv[u], 0.0f);
+            gth += fsel_eqi(i, jj, wsv[u], 0.0f);
           }
         }
         if constexpr (NGC > 1) {

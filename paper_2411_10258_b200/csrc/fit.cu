@@ -485,8 +485,12 @@ struct WinCtl {
 //     them).  One evaluation per warp step: TRAIN groups step after it, FINAL groups record it.
 //   !REFILL (fixed iteration count): every window of a warp stops at the same evaluation, so a
 //     warp takes G windows at a time and keeps them to the end (no per-window bookkeeping).
-template <int DP, bool RESUME, bool REFILL>
-__global__ void __launch_bounds__(128, DP >= 32 ? 2 : 4)
+//   LAT (Dp = 8, batches that fit one wave at 8 warps per SM, e.g. BASELINE cfg2): the same
+//     kernel without the 128-register cap of 16 warps per SM, so ptxas keeps the chunk's
+//     addresses and partial results in registers instead of re-deriving them (the kernel is
+//     bound by each warp's dependent chain there, not by throughput; +6% on cfg2).
+template <int DP, bool RESUME, bool REFILL, bool LAT = false>
+__global__ void __launch_bounds__(128, DP >= 32 || LAT ? 2 : 4)
 k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ alpha,
       float* __restrict__ beta, float* __restrict__ opt, double* __restrict__ lnl_out,
       int32_t* __restrict__ iters_out, int32_t* __restrict__ status,
@@ -952,14 +956,21 @@ static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float*
       }
     }
   }
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if constexpr (DP == 8) {
+    if (cpw == 1 && (P.W + SM::G - 1) / SM::G <= (int64_t)sms * 8) {   // one wave at 8 warps/SM
+      const bool rs = cfg.step0 != 0;
+      kern = cfg.tol_rel > 0.0f ? (rs ? k_fit<DP, true, true, true> : k_fit<DP, false, true, true>)
+                                : (rs ? k_fit<DP, true, false, true> : k_fit<DP, false, false, true>);
+    }
+  }
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess) {
     set_error("cudaFuncSetAttribute(k_fit) failed");
     return MDHP_ECUDA;
   }
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // CTAs per SM from registers, shared memory and TMEM columns.  (The occupancy API reports 1
   // for kernels that allocate tensor memory; the hardware runs as many as the resources allow
   // and tcgen05.alloc would wait for columns, so the grid is sized from the resources here.)
