@@ -542,6 +542,17 @@ __device__ __forceinline__ void event_loop(const float2* __restrict__ A, float2*
   auto co = [&](int off) { return off < npadn ? off : npad; };
   Chunk c0, c1;
   load_chunk(c0, tw, dw, mw, co(0));
+  if constexpr (TC) {
+    // one chunk per iteration: the time-chunked kernel runs twice the warps over two hot loops
+    // (phase 1 and this one), and a two-chunk body left a third of its issue slots waiting on
+    // instruction fetch (ncu "no_instruction", profiles/r02_cfg2_tc*)
+    for (int base = 0; base < nmax; base += 8) {
+      load_chunk(c1, tw, dw, mw, co(base + 8));
+      process_chunk<DP, GRAD, PRE, TC>(c0, A, SQ, Gs, j, gbase, th, last, gth, lsum, tb);
+      c0 = c1;
+    }
+    return;
+  }
   for (int base = 0; base < nmax; base += 16) {
     load_chunk(c1, tw, dw, mw, co(base + 8));
     process_chunk<DP, GRAD, PRE, TC>(c0, A, SQ, Gs, j, gbase, th, last, gth, lsum, tb);
@@ -552,55 +563,75 @@ __device__ __forceinline__ void event_loop(const float2* __restrict__ A, float2*
   }
 }
 
-// The column-update recurrence alone (phase 1 of a time-chunked window, k_fit_tc): from the
-// state in SQ (zero), every event of the chunk re-anchors its column; returns via `last` the
-// time of the latest event of source j (last0 if none).  Loads as event_loop (clampo, tb).
-template <int DP, bool PRE>
-__device__ __forceinline__ void local_loop(const float2* __restrict__ A, float2* __restrict__ SQ,
-                                           const int j, const float* __restrict__ t32,
-                                           const float* __restrict__ dtp,
-                                           const uint8_t* __restrict__ mk, const int64_t beg,
-                                           const int n, const int nmax, float& last,
-                                           const float last0, const int clampo, const float tb) {
+// Phase 1 of a time-chunked window (k_fit_tc): the chunk's local state at its last event te,
+// from an empty history, as direct sums instead of the column recurrence:
+//   S_ji(te) = sum_{k in chunk, mark i} 2^{beta'_ji (te - t_k)},  Q'_ji(te) = sum (te - t_k) 2^{..}
+// -- the lazy recurrence's state re-anchored at te, exact up to rounding, with the same one
+// exponential per event and lane.  The terms are independent (no event-to-event chain: the
+// recurrence made this phase as slow as the full evaluation), so lane j accumulates its row j
+// through the NGC copies of G (scratch here; zeroed by reset_state, re-zeroed for phase 3),
+// NGC events at a time, and finally writes the copies' sum into SQ.  Loads as event_loop.
+template <int DP>
+__device__ __forceinline__ void local_direct(const float2* __restrict__ A, float2* __restrict__ SQ,
+                                             float2* __restrict__ Gs, const int j,
+                                             const float* __restrict__ t32,
+                                             const float* __restrict__ dtp,
+                                             const uint8_t* __restrict__ mk, const int64_t beg,
+                                             const int n, const int nmax, const float te,
+                                             const int clampo) {
   using SM = Smem<DP>;
-  constexpr bool SW = SM::SW;
-  constexpr int kSQ = SM::AS * 8;
-  last = last0;
+  static_assert(SM::SW, "time chunks: Dp <= 8");
+  constexpr int NGC = SM::NGC;
+  constexpr int kG = 2 * SM::AS * 8;
   uint32_t sA = static_cast<uint32_t>(__cvta_generic_to_shared(A));
   asm volatile("" : "+r"(sA) :: "memory");   // see process_chunk
-  const uint32_t colb = SW ? sA + 128u * j : sA + 8u * SM::RS * j;
+  const uint32_t colb = sA + 128u * j;
   const uint32_t colbb = colb + (ab_swapped<DP>(j) ? 0u : 4u);
+  const uint32_t J4 = (uint32_t)j * 0x01010101u;
+  constexpr uint32_t M4 = (uint32_t)(DP - 1) * 0x01010101u;
   const float* tw = t32 + beg;
   const float* dw = dtp + beg;
   const uint8_t* mw = mk + beg;
   auto run8 = [&](const Chunk& ck) {
+    const uint32_t xw[2] = {((ck.mm.x ^ J4) & M4) << 3, ((ck.mm.y ^ J4) & M4) << 3};
 #pragma unroll
-    for (int s = 0; s < 8; s++) {
-      const float t = s == 0 ? ck.ta.x : s == 1 ? ck.ta.y : s == 2 ? ck.ta.z : s == 3 ? ck.ta.w
-                    : s == 4 ? ck.tb.x : s == 5 ? ck.tb.y : s == 6 ? ck.tb.z : ck.tb.w;
-      float dc = s == 0 ? ck.da.x : s == 1 ? ck.da.y : s == 2 ? ck.da.z : s == 3 ? ck.da.w
-               : s == 4 ? ck.db.x : s == 5 ? ck.db.y : s == 6 ? ck.db.z : ck.db.w;
-      dc = fminf(dc, t - tb);
-      const int i = (int)__byte_perm(s < 4 ? ck.mm.x : ck.mm.y, 0u, 0x4440u | (unsigned)(s & 3));
-      MDHP_ASSERT(i >= 0 && i <= DP);
-      const uint32_t x = SW ? (((uint32_t)(i ^ j) & (uint32_t)(DP - 1)) << 3) : ((uint32_t)i << 3);
-      const float bc = lda1o<0>(colbb + x);
-      const float2 sc = lds2o<kSQ>(colb + x);
-      const float ec = PRE ? ex2f(bc * dc) : ex2f(bc * (dc * -kLog2e));
-      if (!SW || i < DP) sts2o<kSQ>(colb + x, fmaf(ec, sc.x, 1.0f), ec * fmaf(dc, sc.x, sc.y));
-      last = fsel_eqi(i, j, t, last);
+    for (int s0 = 0; s0 < 8; s0 += NGC) {
+      uint32_t ga[NGC];
+      float2 gg[NGC];
+      float cv[NGC], dv[NGC];
+      bool real[NGC];
+#pragma unroll
+      for (int u = 0; u < NGC; u++) {
+        const int s = s0 + u;
+        const float t = s == 0 ? ck.ta.x : s == 1 ? ck.ta.y : s == 2 ? ck.ta.z : s == 3 ? ck.ta.w
+                      : s == 4 ? ck.tb.x : s == 5 ? ck.tb.y : s == 6 ? ck.tb.z : ck.tb.w;
+        const int i = (int)__byte_perm(s < 4 ? ck.mm.x : ck.mm.y, 0u, 0x4440u | (unsigned)(s & 3));
+        MDHP_ASSERT(i >= 0 && i <= DP);
+        const uint32_t x = __byte_perm(xw[s >> 2], 0u, 0x4440u | (unsigned)(s & 3));
+        real[u] = i < DP;   // the null column has no storage (SW)
+        dv[u] = te - t;
+        cv[u] = ex2f(lda1o<0>(colbb + x) * dv[u]);
+        ga[u] = colb + x + kG + 8u * (uint32_t)(u * SM::GS);
+        MDHP_ASSERT(ga[u] + 8 <= sA + 8u * (uint32_t)(2 * SM::AS + NGC * SM::GS));
+        gg[u] = lds2(ga[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < NGC; u++)
+        if (real[u]) sts2o<0>(ga[u], gg[u].x + cv[u], fmaf(dv[u], cv[u], gg[u].y));
     }
   };
   const int npadn = (n + 7) & ~7;
   auto co = [&](int off) { return off < npadn ? off : clampo; };
   Chunk c0, c1;
   load_chunk(c0, tw, dw, mw, co(0));
-  for (int base = 0; base < nmax; base += 16) {
+  for (int base = 0; base < nmax; base += 8) {
     load_chunk(c1, tw, dw, mw, co(base + 8));
     run8(c0);
-    load_chunk(c0, tw, dw, mw, co(base + 16));
-    run8(c1);
+    c0 = c1;
   }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < DP; i++) SQ[SM::e(j, i)] = gsum<DP>(Gs, j, i);
   __syncwarp();
 }
 

@@ -637,8 +637,8 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
 // is ~C times shorter.  C = 32/Dp (one window per warp) is the latency mode for single windows
 // (BASELINE cfg1); smaller C trades chain length against windows per warp for small batches.
 // Per evaluation (the a7 chunked scan inside a warp):
-//   phase 1: every group runs its chunk's column updates from a zero state (local_loop) and
-//            re-anchors the local state at the chunk's last event t_e;
+//   phase 1: every group sums its chunk's local state at the chunk's last event t_e from an
+//            empty history (local_direct: direct sums, no recurrence chain);
 //   scan:    the affine maps of a window's chunks (decay over the chunk span + local state,
 //            seq.cu AffMap) are scanned across its groups with warp shuffles; the state carried
 //            into chunk q is the composite of chunks 0..q-1, anchored at the chunk base t_b (the
@@ -705,26 +705,22 @@ __device__ __forceinline__ double eval_window_tc(const Packed& P, float2* A, flo
   const int64_t beg = live ? P.begin[w] : 0;
   const int n = live ? ch.n : 0;
   const int nmax = group_max_i<DP>(n);
-  // ---- phase 1: the chunk's column updates from a zero state
+  // ---- phase 1: the chunk's local state at its last event te (direct sums, local_direct)
   reset_state<DP>(SQ, Gs, c.j);
   __syncwarp();
-  float lastl;
-  local_loop<DP, true>(A, SQ, c.j, P.t32, P.dtp, P.mark, beg + ch.b, n, nmax, lastl, ch.tb,
-                       ch.clampo, ch.tb);
-  // ---- local state at the chunk end (anchor te), as this chunk's affine map per pair (r, j)
+  local_direct<DP>(A, SQ, Gs, c.j, P.t32, P.dtp, P.mark, beg + ch.b, n, nmax, ch.te, ch.clampo);
+  // ---- this chunk's affine map per pair (r, j): decay over the span, local state at te
   TcMap m[DP];
   const float L = ch.te - ch.tb;
-  const float dl = ch.te - lastl;
 #pragma unroll
   for (int r = 0; r < DP; r++) {
     const float2 k = A[SM::e(r, c.j)];
     const float b = ab_beta<DP>(r, k);   // beta' (A holds -beta log2 e)
     const float2 sq = SQ[SM::e(r, c.j)];
-    const float e = ex2f(b * dl);
     m[r].E = ex2f(b * L);
     m[r].L = L;
-    m[r].Sb = e * sq.x;
-    m[r].Qb = e * fmaf(dl, sq.x, sq.y);
+    m[r].Sb = sq.x;
+    m[r].Qb = sq.y;
   }
   // ---- inclusive scan of the maps over the window's groups (lane j of chunk q <- q - k)
 #pragma unroll
