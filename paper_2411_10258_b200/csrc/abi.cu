@@ -442,6 +442,7 @@ int mdhp_seq_loglik_grad(const mdhp_seq_desc* d, const void* packed, const float
     set_error("g_theta, g_alpha, g_beta must be all NULL or all non-NULL");
     return MDHP_EINVAL;
   }
+  keep_pool_memory();
   rc = seq_loglik_launch(d->D, d->n_events, d->chunk_events, d->T, packed, theta, alpha, beta,
                          loglik, g_theta, g_alpha, g_beta, (cudaStream_t)stream);
   if (rc) {
@@ -462,6 +463,7 @@ int mdhp_seq_fit(const mdhp_seq_desc* d, const void* packed, const mdhp_fit_conf
     set_error("NULL pointer argument");
     return MDHP_EINVAL;
   }
+  keep_pool_memory();
   rc = seq_fit_launch(d->D, d->n_events, d->chunk_events, d->T, packed, to_dev(cfg), theta, alpha,
                       beta, opt_state, loglik, iters, status, lnl_trace, (cudaStream_t)stream);
   if (rc) {

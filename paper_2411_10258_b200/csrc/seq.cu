@@ -4,8 +4,8 @@
 // The recurrence state of Eq.(2) for every pair (i, j) evolves between events as a
 // linear map: over a gap L, S <- e^{-beta L} S and Q <- e^{-beta L}(Q + L S), and an event of
 // source j adds 1 to S_.j.  So a long sequence can be cut into chunks (never inside a tie group):
-//   phase 1 (k_seq_local)  every chunk runs its column updates from a zero state -> its local
-//                          state at its last event (2 D^2 floats);
+//   phase 1 (k_seq_local)  every chunk's local state at its last event from an empty
+//                          history, as direct sums (2 D^2 floats);
 //   phase 2 (k_seq_scan)   exclusive scan of the affine maps (decay over the chunk span + local
 //                          state), segmented over chunks, per pair -> the state carried into each
 //                          chunk, anchored at the chunk base (the previous chunk's last event);
@@ -312,7 +312,14 @@ struct SeqCtl {
   double lnl_prev, lnl_last;
 };
 
-// Phase 1: column updates only, from a zero state; local state converted to the chunk end.
+// Phase 1: every chunk's local state at its last event (chunk-relative time Lc), from an
+// empty history, as direct sums instead of the column recurrence (as local_direct in eval.cuh):
+//   S_ji(Lc) = sum_{k in chunk, mark i} e^{-beta_ji (Lc - t_k)},  Q_ji(Lc) = sum (Lc - t_k) e^{..}
+// -- the recurrence's state re-anchored at Lc, exact up to rounding, one exponential per event
+// and lane as before.  The terms are independent, so lane j accumulates its row j (private to
+// the lane: no warp barrier per event) through kLocNC copies, kLocNC events at a time, instead
+// of a load -> FMA -> store chain through every event.
+constexpr int kLocNC = 2;
 template <int DP>
 __global__ void __launch_bounds__(128)
 k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t* __restrict__ cbeg,
@@ -320,30 +327,32 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
             const float* __restrict__ dtp, const uint8_t* __restrict__ mk,
             const float* __restrict__ beta, float2* __restrict__ loc, const int* __restrict__ ctl) {
   if (ctl && ctl[0]) return;
-  constexpr int G = 32 / DP, RS = DP + 1;
+  constexpr int G = 32 / DP, RS = DP + 1, CS = DP * RS;   // CS: float2 per copy
   extern __shared__ __align__(16) unsigned char smem_l[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / DP, j = lane % DP;
-  float2* SQ = reinterpret_cast<float2*>(smem_l) + (size_t)(wid * G + g) * DP * RS;
-  float* B = reinterpret_cast<float*>(reinterpret_cast<float2*>(smem_l) + (size_t)4 * G * DP * RS) +
-             (size_t)(wid * G + g) * DP * RS;
+  float2* SQ = reinterpret_cast<float2*>(smem_l) + (size_t)(wid * G + g) * kLocNC * CS;
+  float* B = reinterpret_cast<float*>(reinterpret_cast<float2*>(smem_l) + (size_t)4 * G * kLocNC * CS) +
+             (size_t)(wid * G + g) * CS;
   const int64_t c = ((int64_t)blockIdx.x * 4 + wid) * G + g;
   const bool live = c < C;
   const int n = live ? (int)(cstart[c + 1] - cstart[c]) : 0;
-  // lane = column here (coalesced rows of beta): B[r][j] = beta_rj, SQ[r][j] = 0
+  // lane = column here (coalesced rows of beta): B[r][j] = beta_rj, SQ copies [r][j] = 0
   for (int r = 0; r < DP; r++) {
-    SQ[r * RS + j] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int k = 0; k < kLocNC; k++) SQ[k * CS + r * RS + j] = make_float2(0.0f, 0.0f);
     if (r < D && j < D) cp_async<4>(&B[r * RS + j], beta + (size_t)r * D + j);
     else B[r * RS + j] = 0.0f;
   }
   cp_async_wait_all();
   // column DP: the null event's (never read) column
-  SQ[j * RS + DP] = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int k = 0; k < kLocNC; k++) SQ[k * CS + j * RS + DP] = make_float2(0.0f, 0.0f);
   B[j * RS + DP] = 0.0f;
   __syncwarp();
   int nmax = n;
   for (int o = 16; o >= 1; o >>= 1) nmax = max(nmax, __shfl_xor_sync(kFull, nmax, o));
   const int64_t beg = live ? cbeg[c] : 0;
-  float last = -1.0f;
+  const float Lc = live ? cspan[c] : 0.0f;
   // 8 events per vector load (the chunk layout is the window layout: 8-aligned, padded with
   // null events up to a multiple of 8 plus one null chunk), the next chunk prefetched
   const float* tw = t32 + beg;
@@ -352,18 +361,24 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
   const int npad = (n + 7) & ~7;
   auto local8 = [&](const Chunk& ck) {
 #pragma unroll
-    for (int s = 0; s < 8; s++) {
-      const float t = s == 0 ? ck.ta.x : s == 1 ? ck.ta.y : s == 2 ? ck.ta.z : s == 3 ? ck.ta.w
-                    : s == 4 ? ck.tb.x : s == 5 ? ck.tb.y : s == 6 ? ck.tb.z : ck.tb.w;
-      const float dc = s == 0 ? ck.da.x : s == 1 ? ck.da.y : s == 2 ? ck.da.z : s == 3 ? ck.da.w
-                     : s == 4 ? ck.db.x : s == 5 ? ck.db.y : s == 6 ? ck.db.z : ck.db.w;
-      const int i = (int)__byte_perm(s < 4 ? ck.mm.x : ck.mm.y, 0u, 0x4440u | (unsigned)(s & 3));
-      MDHP_ASSERT(i >= 0 && i <= DP);   // DP: null event (gap 0, beta 0: a no-op on column DP)
-      const float2 sv = SQ[j * RS + i];
-      const float e = ex2f(B[j * RS + i] * (dc * -kLog2e));
-      SQ[j * RS + i] = make_float2(fmaf(e, sv.x, 1.0f), e * fmaf(dc, sv.x, sv.y));
-      last = fsel_eqi(i, j, t, last);
-      __syncwarp();
+    for (int s0 = 0; s0 < 8; s0 += kLocNC) {
+      float2 v[kLocNC];
+      float cv[kLocNC], dv[kLocNC];
+      int ad[kLocNC];
+#pragma unroll
+      for (int u = 0; u < kLocNC; u++) {
+        const int s = s0 + u;
+        const float t = s == 0 ? ck.ta.x : s == 1 ? ck.ta.y : s == 2 ? ck.ta.z : s == 3 ? ck.ta.w
+                      : s == 4 ? ck.tb.x : s == 5 ? ck.tb.y : s == 6 ? ck.tb.z : ck.tb.w;
+        const int i = (int)__byte_perm(s < 4 ? ck.mm.x : ck.mm.y, 0u, 0x4440u | (unsigned)(s & 3));
+        MDHP_ASSERT(i >= 0 && i <= DP);   // DP: null event (beta 0: adds to the unread column DP)
+        dv[u] = Lc - t;
+        cv[u] = ex2f(B[j * RS + i] * (dv[u] * -kLog2e));
+        ad[u] = u * CS + j * RS + i;
+        v[u] = SQ[ad[u]];
+      }
+#pragma unroll
+      for (int u = 0; u < kLocNC; u++) SQ[ad[u]] = make_float2(v[u].x + cv[u], fmaf(dv[u], cv[u], v[u].y));
     }
   };
   Chunk c0, c1;
@@ -374,19 +389,17 @@ k_seq_local(int D, int64_t C, const int64_t* __restrict__ cstart, const int64_t*
     load_chunk(c0, tw, dw, mw, min(base + 16, npad));
     local8(c1);
   }
-  // local state at the chunk end, written row by row with lane = column (coalesced): lane j
-  // holds last_j, the anchor of column j
-  const float Lc = live ? cspan[c] : 0.0f;
+  // local state at the chunk end, written row by row with lane = column (coalesced); element
+  // (r, j) was accumulated by lane r
   __syncwarp();
   for (int r = 0; r < D; r++) {
     if (live && j < D) {
       float2 s = SQ[r * RS + j];
-      if (last >= 0.0f) {
-        const float dl = Lc - last;
-        const float e = ex2f(B[r * RS + j] * (dl * -kLog2e));
-        s = make_float2(e * s.x, e * fmaf(dl, s.x, s.y));
-      } else {
-        s = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int k = 1; k < kLocNC; k++) {
+        const float2 x = SQ[k * CS + r * RS + j];
+        s.x += x.x;
+        s.y += x.y;
       }
       loc[(size_t)c * D * D + (size_t)r * D + j] = s;
     }
@@ -918,7 +931,7 @@ static void seq_phases_t(const SeqLayout& L, const void* pk, const float* th, co
   if (C == 0) return;
   constexpr int G = 32 / DP;
   const unsigned blk = (unsigned)((C + 4 * G - 1) / (4 * G));
-  const size_t lsm = (size_t)4 * G * DP * (DP + 1) * (sizeof(float2) + sizeof(float));
+  const size_t lsm = (size_t)4 * G * DP * (DP + 1) * (kLocNC * sizeof(float2) + sizeof(float));
   if (!sd.skip_local) {
     k_seq_local<DP><<<blk, 128, lsm, st>>>(L.D, C, at<int64_t>(pk, L.cstart), at<int64_t>(pk, L.cbeg),
                                          at<float>(pk, L.cspan), at<float>(pk, L.t32),
@@ -946,7 +959,7 @@ static void seq_phases_t(const SeqLayout& L, const void* pk, const float* th, co
 template <int DP>
 static void seq_set_attrs_t() {
   constexpr int G = 32 / DP;
-  const size_t lsm = (size_t)4 * G * DP * (DP + 1) * (sizeof(float2) + sizeof(float));
+  const size_t lsm = (size_t)4 * G * DP * (DP + 1) * (kLocNC * sizeof(float2) + sizeof(float));
   cudaFuncSetAttribute(k_seq_local<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
   cudaFuncSetAttribute(k_seq_eval<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(4 * Smem<DP>::per_warp));
