@@ -329,11 +329,12 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
   const uint32_t colbb = colb + (ab_swapped<DP>(j) ? 0u : 4u);
   float pv[8], Rv[8], Qv[8];
   float lacc = 0.0f;
-  // DP <= 8 (latency-bound: few warps per SM): the column decay factors ec of the chunk's 8
-  // events depend only on parameters (beta'_ji) and gaps, so their loads and exponentials are
-  // issued here, ahead of the chunk's state stores, which takes the beta load and the MUFU off
-  // the event-to-event chain (state load -> FFMA -> state store).  (ptxas cannot move the
-  // loads above the stores itself: it cannot prove the addresses disjoint.)
+  // DP <= 8 and DP = 32 (latency-bound: few warps per SM): the column decay factors ec of the
+  // chunk's 8 events depend only on parameters (beta'_ji) and gaps, so their loads and
+  // exponentials are issued here, ahead of the chunk's state stores, which takes the beta load
+  // and the MUFU off the event-to-event chain (state load -> FFMA -> state store).  (ptxas
+  // cannot move the loads above the stores itself: it cannot prove the addresses disjoint.)
+  // cfg3 (DP = 32) +4.6%; DP = 16 (bound by the shared-memory slot, not latency) unchanged.
   // SW: the addresses of the chunk's 8 events come from two byte-parallel words per 4 events:
   // y = 16 i + ((i ^ j) & (DP-1)) (the row element (i, j) in float2 units from the group base,
   // <= 135, one byte) and x = 8 ((i ^ j) & (DP-1)) (the column element's byte offset), so an
@@ -353,7 +354,7 @@ __device__ __forceinline__ void process_chunk(const Chunk& ck, const float2* __r
     }
   }
   auto byte_of = [](uint32_t w, int s) -> uint32_t { return __byte_perm(w, 0u, 0x4440u | (unsigned)(s & 3)); };
-  constexpr bool HOIST = DP <= 8;
+  constexpr bool HOIST = DP <= 8 || DP == 32;
   float ecs[8];
   if constexpr (HOIST) {
 #pragma unroll
