@@ -245,6 +245,8 @@ struct FitCfgDev {
   unsigned fit_mask;
   int step0;   // Adam steps of earlier calls (resume)
   int time_chunks;   // time chunks per window (k_fit_tc), 0/1 = throughput layout
+  int slot_order = 0;   // launcher-internal (k_fit LAT, fixed iterations): 1 = static unit per
+                        // warp slot, longest units alone on their SM sub-partition
 };
 
 // launch counter (process-wide), incremented by every launch site

@@ -488,9 +488,15 @@ struct WinCtl {
 //   LAT (Dp = 8, batches that fit one wave at 8 warps per SM, e.g. BASELINE cfg2): the same
 //     kernel without the 128-register cap of 16 warps per SM, so ptxas keeps the chunk's
 //     addresses and partial results in registers instead of re-deriving them (the kernel is
-//     bound by each warp's dependent chain there, not by throughput; +6% on cfg2).
+//     bound by each warp's dependent chain there, not by throughput; +6% on cfg2).  With fixed
+//     iterations it runs one CTA of 8 warps per SM and cfg.slot_order = 1: warp slot (CTA b,
+//     warp w) takes unit order(w) * gridDim + b, order = 0 for warp 0, 1-6 for warps 1-3 and
+//     5-7, 7 for warp 4, so the gridDim longest units (perm is longest-first) run on warp 0 of
+//     every SM with no other busy warp on its sub-partition (warps w and w+4 share one), and
+//     the batch time -- set by the warps holding the longest windows -- approaches their
+//     uncontended chain (profiles/r02_cfg2_latency_profiles.txt).
 template <int DP, bool RESUME, bool REFILL, bool LAT = false>
-__global__ void __launch_bounds__(128, DP >= 32 || LAT ? 2 : 4)
+__global__ void __launch_bounds__(LAT ? 256 : 128, DP >= 32 ? 2 : LAT ? 1 : 4)
 k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ alpha,
       float* __restrict__ beta, float* __restrict__ opt, double* __restrict__ lnl_out,
       int32_t* __restrict__ iters_out, int32_t* __restrict__ status,
@@ -506,8 +512,10 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
   float2* SQ = gbase_s + SM::AS;
   float2* Gs = gbase_s + 2 * SM::AS;
   uint32_t* slot = reinterpret_cast<uint32_t*>(smem + (blockDim.x >> 5) * SM::per_warp);
-  const uint32_t tbase = tm_alloc(slot, TL::ALLOC);
-  const uint32_t tm = tbase + ((uint32_t)((wid & 3) * 32) << 16);
+  // warps w and w + 4 of an 8-warp CTA share TMEM lanes 32 (w % 4) ..: separate column blocks
+  const uint32_t tcols = TL::ALLOC * (blockDim.x > 128 ? 2u : 1u);
+  const uint32_t tbase = tm_alloc(slot, tcols);
+  const uint32_t tm = tbase + ((uint32_t)((wid & 3) * 32) << 16) + (uint32_t)(wid >> 2) * TL::ALLOC;
   const int D = P.D;
   if constexpr (REFILL) {
     enum { TRAIN = 0, FINAL = 1, IDLE = 2 };
@@ -582,10 +590,18 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
     }
   } else {
     const int64_t nunits = (P.W + SM::G - 1) / SM::G;
+    bool taken = false;
     for (;;) {
       int64_t unit = 0;
-      if (c.lane == 0) unit = atomicAdd(counter, 1);
-      unit = __shfl_sync(kFull, unit, 0);
+      if (LAT && cfg.slot_order) {   // one static unit per warp slot (see above)
+        if (taken) break;
+        taken = true;
+        const int order = wid == 0 ? 0 : wid < 4 ? wid : wid > 4 ? wid - 1 : 7;
+        unit = (int64_t)order * gridDim.x + blockIdx.x;
+      } else {
+        if (c.lane == 0) unit = atomicAdd(counter, 1);
+        unit = __shfl_sync(kFull, unit, 0);
+      }
       if (unit >= nunits) break;
       const int64_t slot_w = unit * SM::G + c.g;
       const int64_t w = slot_w < P.W ? P.perm[slot_w] : 0;
@@ -627,7 +643,7 @@ k_fit(Packed P, FitCfgDev cfg, float* __restrict__ theta, float* __restrict__ al
       __syncwarp();
     }
   }
-  tm_free(tbase, TL::ALLOC);
+  tm_free(tbase, tcols);
 }
 
 // ---------------------------------------------------------------- time chunks (latency mode)
@@ -955,11 +971,27 @@ static int launch_fit_t(const Packed& P, const FitCfgDev& cfg, float* th, float*
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  FitCfgDev kc = cfg;
   if constexpr (DP == 8) {
-    if (cpw == 1 && (P.W + SM::G - 1) / SM::G <= (int64_t)sms * 8) {   // one wave at 8 warps/SM
+    const int64_t u8 = (P.W + SM::G - 1) / SM::G;
+    if (cpw == 1 && u8 <= (int64_t)sms * 8) {   // one wave at 8 warps/SM
       const bool rs = cfg.step0 != 0;
       kern = cfg.tol_rel > 0.0f ? (rs ? k_fit<DP, true, true, true> : k_fit<DP, false, true, true>)
                                 : (rs ? k_fit<DP, true, false, true> : k_fit<DP, false, false, true>);
+      // fixed iterations, at most 7 units per SM: one 8-warp CTA per SM with the static
+      // sub-partition-aware unit order (k_fit LAT)
+      if (cfg.tol_rel <= 0.0f && u8 <= (int64_t)sms * 7 && !getenv("MDHP_NO_SLOT_ORDER")) {
+        const size_t smem8 = 8 * SM::per_warp + 16;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8) != cudaSuccess) {
+          set_error("cudaFuncSetAttribute(k_fit) failed");
+          return MDHP_ECUDA;
+        }
+        kc.slot_order = 1;
+        kern<<<(unsigned)sms, 256, smem8, st>>>(P, kc, th, al, be, opt, lnl, iters, status, trace, counter,
+                                               xlist, xcount);
+        count_launch();
+        return MDHP_OK;
+      }
     }
   }
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=

@@ -43,7 +43,7 @@ def timed(D, t, m, off, T, cfg, reps=3):
 b = sg.make_batch_gpu("cfg2", 4096, seed=2024)
 D = b["D"]
 n = (b["win_off"][1:] - b["win_off"][:-1]).cpu().numpy()
-cfg = M.FitConfig(max_iters=500, optimizer="adam", lr=0.05)
+cfg = M.FitConfig(max_iters=500, optimizer="adam", lr=0.05, tol_rel=0.0)
 allw = np.arange(len(n))
 print(f"windows {len(n)} events mean {n.mean():.1f} max {n.max()}")
 print(f"all: {timed(D, *subset(b, allw), cfg):.2f} ms")
