@@ -2,7 +2,9 @@
 ranges, each range packed and fitted on its own, must give the N = 1 results bit for bit -- a
 window's fit never depends on which other windows share its launch.  The cfg2 8192-window
 cases also pin the two k_fit<8> builds against each other: the full batch (2,048 warp units)
-runs the 16-warps/SM kernel, its ranges (<= 1,184 units) the one-wave LAT kernel (fit.cu)."""
+runs the 16-warps/SM kernel, its ranges (<= 1,184 units) the one-wave LAT kernel (fit.cu) with
+the static sub-partition-aware unit order (<= 7 units per SM); cfg2 4500 (1,125 units) runs the
+LAT kernel with the dynamic order, its ranges the static one."""
 import numpy as np
 import pytest
 import torch
@@ -25,7 +27,7 @@ def _fit(D, t, m, off, T, cfg):
 
 
 @pytest.mark.parametrize("cfg_name,W,tol", [("cfg5", 8192, 0.0), ("cfg2", 4096, 0.0), ("cfg5", 4096, 1e-4),
-                                              ("cfg2", 8192, 0.0), ("cfg2", 8192, 1e-4)])
+                                              ("cfg2", 8192, 0.0), ("cfg2", 8192, 1e-4), ("cfg2", 4500, 0.0)])
 def test_ranges_concat_equal_single_gpu(cfg_name, W, tol):
     b = sg.make_batch_gpu(cfg_name, W, seed=2024)
     D = b["D"]
