@@ -10,14 +10,15 @@
 #include <cuda_runtime.h>
 #define CK(x) do{cudaError_t e=(x); if(e!=cudaSuccess){printf("ERR %s line %d\n",cudaGetErrorString(e),__LINE__);return 1;}}while(0)
 
-template <int BYTES, bool SHARED>
+template <int BYTES, bool SHARED, bool SAMELINE = false>
 __global__ void k_ld(const float4* __restrict__ g, float* out, int iters) {
   extern __shared__ float4 sm[];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int i = tid; i < 2048; i += blockDim.x) sm[i] = make_float4(i, i, i, i);
   __syncthreads();
   // group = lane / 16: two distinct 16-byte records per warp, in different 128-byte lines
-  const int base = (w * 64 + (lane >> 4) * 8) & 1023;
+  // SAMELINE: the two groups' records 32 bytes apart, in one 128-byte line
+  const int base = (w * 64 + (lane >> 4) * (SAMELINE ? 2 : 8)) & 1023;
   float acc = 0.0f;
   for (int it = 0; it < iters; it++) {
 #pragma unroll
@@ -44,16 +45,16 @@ __global__ void k_ld(const float4* __restrict__ g, float* out, int iters) {
   if (acc == 1.2345f) out[0] = acc;
 }
 
-template <int BYTES, bool SHARED>
+template <int BYTES, bool SHARED, bool SAMELINE = false>
 int run(const float4* g, float* out, int sms, const char* name) {
   const int threads = 256, iters = 4096, blocks = sms * 4;   // 32 warps per SM
-  CK(cudaFuncSetAttribute(k_ld<BYTES, SHARED>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768));
+  CK(cudaFuncSetAttribute(k_ld<BYTES, SHARED, SAMELINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   for (int rep = 0; rep < 2; rep++) {
     cudaEventRecord(e0);
-    k_ld<BYTES, SHARED><<<blocks, threads, 32768>>>(g, out, iters);
+    k_ld<BYTES, SHARED, SAMELINE><<<blocks, threads, 32768>>>(g, out, iters);
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -78,5 +79,8 @@ int main() {
   run<16, false>(g, out, sms, "LDG.128 (L1 hit), 2 distinct addresses");
   run<8, false>(g, out, sms, "LDG.64  (L1 hit), 2 distinct addresses");
   run<4, false>(g, out, sms, "LDG.32  (L1 hit), 2 distinct addresses");
+  run<16, false, true>(g, out, sms, "LDG.128 (L1 hit), 2 addresses in one line");
+  run<8, false, true>(g, out, sms, "LDG.64  (L1 hit), 2 addresses in one line");
+  run<16, true, true>(g, out, sms, "LDS.128, 2 addresses 32 B apart");
   return 0;
 }
