@@ -598,8 +598,19 @@ int mdhp_fit_host(const mdhp_pack_desc* d, const double* t_h, const int32_t* mar
   // overlap the fit of part p-1 (the caller's stream) and its results go back while part p+1
   // fits, so the end-to-end time is one part's upload + the fits + one part's download.
   // Windows are independent, so the results equal those of one call on the whole batch.
+  // Only batches whose parts are themselves throughput-bound (>= 4 waves of the 16-warps/SM
+  // layout each) are cut: a batch of a few waves is bound by the chains of its longest windows,
+  // and four parts would run four such chains back to back (cfg2: 91 ms per call against the
+  // 26 ms fit).  Time-chunked (latency) fits are never cut.
   constexpr int kHostParts = 4;
-  const int P = W >= 4096 ? kHostParts : 1;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    sms = 148;
+  int Dp = 1;
+  while (Dp < D) Dp <<= 1;
+  const int64_t wave = (int64_t)sms * 16 * (32 / Dp);   // windows in one wave of warps
+  const int P = (cfg->time_chunks < 2 && W / kHostParts >= 4 * wave) ? kHostParts : 1;
   int64_t w0[kHostParts + 1];
   for (int q = 0; q <= P; q++) w0[q] = W * q / P;
   size_t pko[kHostParts + 1];

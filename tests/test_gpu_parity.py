@@ -423,19 +423,25 @@ def test_fit_masks_and_adam_hyperparameters(mask):
                 np.testing.assert_array_equal(g[k][w], f32(start[w]))
 
 
-@pytest.mark.parametrize("pinned", [True, False])
-def test_fit_host_pipelined_parts_equal_device_path(pinned):
-    """mdhp_fit_host with >= 4096 windows cuts the batch into parts whose uploads, fits and
-    downloads overlap on two streams; windows are independent, so every output equals one
-    pack + fit of the whole batch on device buffers, bit for bit (uneven part sizes, empty
-    windows included)."""
+@pytest.mark.parametrize("pinned,split", [(True, True), (False, True), (True, False)])
+def test_fit_host_pipelined_parts_equal_device_path(pinned, split):
+    """mdhp_fit_host cuts a batch whose parts each fill >= 4 waves of warps (abi.cu) into parts
+    whose uploads, fits and downloads overlap on two streams (split); smaller batches run whole.
+    Windows are independent, so every output equals one pack + fit of the whole batch on device
+    buffers, bit for bit (uneven part sizes, empty windows included)."""
     rng = np.random.default_rng(4242)
-    D, W = 3, 4099
-    wins = []
-    for w in range(W):
-        n = int(rng.integers(0, 40)) if w % 97 else 0
-        wins.append((np.sort(rng.uniform(0.0, 1.0, n)), rng.integers(0, D, n).astype(np.int32)))
-    b = H.batch_from_windows(wins, 1.0)
+    D = 3
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    W = 16 * sms * 16 * 8 + 3 if split else 4099   # Dp = 4: 8 windows per warp, 16 warps/SM
+    n = rng.integers(0, 40, W)
+    n[::97] = 0
+    off = np.zeros(W + 1, np.int64)
+    off[1:] = np.cumsum(n)
+    E = int(off[-1])
+    wid = np.repeat(np.arange(W), n)
+    t = rng.uniform(0.0, 1.0, E)
+    t = t[np.lexsort((t, wid))]
+    b = {"t": t, "mark": rng.integers(0, D, E).astype(np.int32), "win_off": off, "T": np.full(W, 1.0)}
     cfg = M.FitConfig(max_iters=8, tol_rel=0.0)
     th = torch.full((W, D), 3.0); al = torch.full((W, D, D), 0.7); be = torch.full((W, D, D), 9.0)
     th_d, al_d, be_d = th.to(DEV), al.to(DEV), be.to(DEV)
